@@ -1,0 +1,49 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: longer-running case")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return np.load(os.path.join(GOLDEN, "golden.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_meta():
+    import json
+
+    with open(os.path.join(GOLDEN, "golden_meta.json")) as fh:
+        return json.load(fh)
+
+
+def golden_case(z, name):
+    from oracle.oracle import Csr
+
+    rp = z[f"{name}/rp"]
+    ci = z[f"{name}/ci"]
+    va = z[f"{name}/va"]
+    rows = rp.size - 1
+    return rp, ci, va, rows
+
+
+@pytest.fixture(scope="session")
+def gpu_available():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
