@@ -1,0 +1,518 @@
+"""bench.py — DA-SpMM on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): the synthetic suite — uniform, banded and
+power-law (R-MAT, Graph500 skew) CSR matrices with 2^14 / 2^17 / 2^20 rows at
+average degree 16 (banded: half-width 8), each multiplied by a dense B of
+N = 2, 4, 8, 16, 32, 64, 128 columns, fp32. One *step* runs DA-SpMM — the on-device
+selector plus the selected sm_100a kernel, dispatched on the device through a CUDA
+graph SWITCH node — once for every (matrix, N) pair of the suite.
+
+  value     suite GFLOP/s = sum(2*nnz*N) / sum(device time), inputs resident in HBM,
+            L2 flushed (256 MiB write) before every call, CUDA events per call.
+  e2e       same metric through the public API with host operands: pinned-host B ->
+            device, DA-SpMM, C -> pinned host, all inside the timed region.
+  roofline  HBM roofline of the step: algorithmic bytes (SURVEY §8d:
+            4(M+1) + 8 nnz + 4 N K_touched + 4 N M per call) / device time, against
+            MEASURED_PEAKS.json hbm_gbs; `dominant` repeats it for the largest call.
+  cpu_baseline  the reference's own spmm() (oracle/_ref, unmodified headers) RB+RM+SR
+            on all host cores over a bounded sample of the suite.
+
+--gpus N (torchrun): every rank takes an nnz-balanced row panel of every matrix
+(partition.hpp cut rule) with B replicated; no collective on the data path; time =
+max over ranks. --impl reference: the reference CPU path alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NS = (2, 4, 8, 16, 32, 64, 128)
+FLUSH_BYTES = 256 << 20
+
+
+# ------------------------------------------------------------------ helpers
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ workload
+def build_suite(small: bool, rank: int, world: int):
+    """Generates the suite on the current device; returns per-matrix dicts holding the
+    rank's row panel as a DeviceCsr."""
+    import torch
+
+    from paper_2202_08556_b200 import gen, multi
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    mats = []
+    for name, mk in gen.suite(small=small):
+        M, K, rp, ci, va = mk()
+        full = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+        if world > 1:
+            cuts = multi.row_panel_cuts(rp.cpu().numpy(), world)
+            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+            d = full.panel(r0, r1)
+            torch.cuda.synchronize()
+        else:
+            r0, r1, d = 0, M, full
+        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), d=d, full=full,
+                         rows=(r0, r1), rp=rp, ci=ci, va=va))
+    return mats
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2202_08556_b200 import gen
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    sk.lib()  # fail loudly if the CUDA library is missing
+    model = sk.load_selector(open(args.model).read())
+    mats = build_suite(args.small, rank, world)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    ns = [int(n) for n in args.ns.split(",")] if args.ns else list(NS)
+
+    # Operands per (matrix, N): B replicated, C local panel.
+    calls = []
+    for m in mats:
+        d = m["d"]
+        for n in ns:
+            B = gen.dense_operand(m["K"], n, seed=1000 + n, device=dev)
+            Cp = torch.empty(d.num_rows, n, device=dev)
+            kout = torch.zeros(1, dtype=torch.int32, device=dev)
+            calls.append(dict(m=m, n=n, B=B, C=Cp, kout=kout,
+                              flops=gen.flops(d.nnz(), n),
+                              bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), n, d.cols_touched)))
+    stream = torch.cuda.current_stream(dev)
+
+    def one(c):
+        sk.spmm_selected(c["m"]["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream)
+
+    def step(times=None):
+        for i, c in enumerate(calls):
+            flush.zero_()
+            if times is None:
+                one(c)
+            else:
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                one(c)
+                e.record(stream)
+                times[i].append((s, e))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    times = [[] for _ in calls]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            step(times)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_call_ms = [sum(s.elapsed_time(e) for s, e in t) / max(args.steps, 1) for t in times]
+    step_ms = sum(per_call_ms)
+    if world > 1:
+        tt = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    total_flops = sum(gen.flops(m["nnz_total"], n) for m in mats for n in ns)
+    value = total_flops / (step_ms * 1e-3) / 1e9
+
+    # kernel choices and launch count (select + [EB prologue] + spmm per call)
+    chosen = [int(c["kout"].item()) for c in calls]
+    launches_per_step = sum(2 + (1 if k >= 4 else 0) for k in chosen)
+
+    # roofline over this rank's calls
+    peak, peak_kind = _peaks()
+    my_bytes = sum(c["bytes"] for c in calls)
+    achieved = my_bytes / (sum(per_call_ms) * 1e-3) / 1e9
+    dom = max(range(len(calls)), key=lambda i: per_call_ms[i])
+    dom_ach = calls[dom]["bytes"] / (per_call_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        key = f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}'
+        traffic = tr.get(key)
+    except Exception:
+        pass
+
+    # ---- e2e: host operands through the public API (pinned H2D, DA-SpMM, D2H)
+    hostB = [c["B"].cpu().pin_memory() for c in calls]
+    hostC = [torch.empty(c["C"].shape, dtype=torch.float32).pin_memory() for c in calls]
+    h2d = sum(b.numel() * 4 for b in hostB)
+    d2h = sum(h.numel() * 4 for h in hostC)
+
+    def e2e_step():
+        for i, c in enumerate(calls):
+            c["B"].copy_(hostB[i], non_blocking=True)
+            one(c)
+            hostC[i].copy_(c["C"], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = s.elapsed_time(e) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = total_flops / (e2e_ms * 1e-3) / 1e9
+
+    # parity spot-check of the timed outputs against the fp64 CPU oracle (rows sample)
+    parity = _spot_check(calls[dom]) if rank == 0 else None
+
+    result = {
+        "metric": "SpMM GFLOP/s (2*nnz*N/t), DA-SpMM over the synthetic suite",
+        "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[1] synthetic suite: uniform/banded/power-law, "
+                               + ("2^14,2^17" if args.small else "2^14,2^17,2^20")
+                               + " rows, deg 16, N=" + ",".join(map(str, ns)),
+                   "matrices": [m["name"] for m in mats], "ns": ns,
+                   "calls_per_step": len(calls), "selector": os.path.basename(args.model),
+                   "l2": "flushed (256 MiB write) before every timed call",
+                   "parallelism": f"row-panels x{world}, B replicated" if world > 1 else "1 GPU"},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "scope": "suite aggregate: sum algorithmic bytes / sum call time",
+                     "dominant": {"call": f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}',
+                                  "kernel": sk.KernelId.from_index(chosen[dom]).name(),
+                                  "ms": round(per_call_ms[dom], 4),
+                                  "achieved": round(dom_ach, 1),
+                                  "frac": round(dom_ach / peak, 4)}},
+        "clocks": clk.summary(),
+        "selected": {f'{c["m"]["name"]}/N{c["n"]}': sk.KernelId.from_index(k).name()
+                     for c, k in zip(calls, chosen)},
+        "per_call_ms": {f'{c["m"]["name"]}/N{c["n"]}': round(t, 5)
+                        for c, t in zip(calls, per_call_ms)},
+        "parity": parity,
+    }
+    if rank == 0 and not args.no_cusparse:
+        result["cusparse"] = _cusparse_compare(calls, flush, per_call_ms, ns)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = _cpu_baseline(mats, ns, steps=1)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _spot_check(c):
+    """fp64 oracle on a sample of rows of the dominant call (gamma bound)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    m = c["m"]
+    r0, r1 = m["rows"]
+    rp = m["rp"].cpu().numpy().astype(np.int64)[r0:r1 + 1]
+    rows = np.unique(np.linspace(0, r1 - r0 - 1, num=min(512, r1 - r0)).astype(np.int64))
+    ci = m["ci"].cpu().numpy().astype(np.int64)
+    va = m["va"].cpu().numpy().astype(np.float64)
+    sub_rp = [0]
+    sub_ci, sub_va = [], []
+    for r in rows:
+        s, e = rp[r], rp[r + 1]
+        sub_ci.append(ci[s:e])
+        sub_va.append(va[s:e])
+        sub_rp.append(sub_rp[-1] + (e - s))
+    a = O.Csr(len(rows), m["K"], np.array(sub_rp), np.concatenate(sub_ci), np.concatenate(sub_va))
+    x = c["B"].cpu().numpy().astype(np.float64)
+    y64 = O.spmm_reference(a, x)
+    absa = O.Csr(a.num_rows, a.num_cols, a.row_offsets, a.col_indices, np.abs(a.values))
+    mag = O.spmm_reference(absa, np.abs(x))
+    lens = np.diff(a.row_offsets).astype(np.float64)
+    u = 2.0 ** -24
+    bound = 2 * ((lens + 1) * u / (1 - (lens + 1) * u))[:, None] * mag + 1e-30
+    y = c["C"].cpu().numpy()[rows].astype(np.float64)
+    ok = bool((np.abs(y - y64) <= bound).all())
+    return {"call": f'{m["name"]}/N{c["n"]}', "rows_checked": int(len(rows)), "within_gamma": ok,
+            "max_abs_err": float(np.abs(y - y64).max()) if y.size else 0.0}
+
+
+def _cusparse_compare(calls, flush, our_ms, ns):
+    """Best of cuSPARSE CSR algorithms per call, same operands, same L2 flush."""
+    import torch
+
+    from paper_2202_08556_b200 import build
+
+    path = build.CUSPARSE_LIB
+    if not os.path.exists(path):
+        return None
+    L = C.CDLL(path)
+    L.cmp_create.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 4 + [C.c_int64] * 2 + \
+        [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.cmp_run.argtypes = [C.c_void_p]
+    L.cmp_destroy.argtypes = [C.c_void_p]
+    stream = torch.cuda.current_stream()
+    best = []
+    for c in calls:
+        d = c["m"]["d"]
+        rp, ci, va = d.device_arrays()
+        out = torch.empty_like(c["C"])
+        ts = {}
+        for alg in (0, 1, 2, 3):
+            h = C.c_void_p()
+            if L.cmp_create(d.num_rows, d.num_cols, d.nnz(), rp, ci, va, c["B"].data_ptr(), c["n"],
+                            c["n"], out.data_ptr(), c["n"], alg, stream.cuda_stream,
+                            C.byref(h)) != 0:
+                continue
+            for _ in range(2):
+                L.cmp_run(h)
+            samples = []
+            for _ in range(3):
+                flush.zero_()
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                L.cmp_run(h)
+                e.record(stream)
+                torch.cuda.synchronize()
+                samples.append(s.elapsed_time(e))
+            ts[alg] = sorted(samples)[1]
+            L.cmp_destroy(h)
+        best.append(min(ts.values()) if ts else float("nan"))
+    tot_flops = sum(c["flops"] for c in calls)
+    cus_ms = sum(best)
+    speedups = [b / o for b, o in zip(best, our_ms) if o > 0]
+    geo = float(statistics.geometric_mean(speedups)) if speedups else None
+    by_n = {}
+    for c, b, o in zip(calls, best, our_ms):
+        by_n.setdefault(c["n"], []).append(b / o)
+    return {"value": round(tot_flops / (cus_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "best_alg_per_call": True, "ms_per_step": round(cus_ms, 4),
+            "speedup_geomean": round(geo, 4) if geo else None,
+            "speedup_geomean_by_N": {str(n): round(statistics.geometric_mean(v), 4)
+                                     for n, v in sorted(by_n.items())}}
+
+
+# ------------------------------------------------------------------ CPU reference
+def _ref_sample(mats, ns):
+    """Bounded sample of the suite for the CPU reference: every 2^14 matrix at
+    every N and every 2^17 matrix at N <= 8."""
+    out = []
+    for m in mats:
+        if m["M"] <= (1 << 14):
+            out += [(m, n) for n in ns]
+        elif m["M"] <= (1 << 17):
+            out += [(m, n) for n in ns if n <= 8]
+    return out
+
+
+def _cpu_time_reference(sample, steps):
+    """Times the reference's spmm() (RB+RM+SR, P = all host cores) via oracle/_ref."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    R = O.ref()
+    if R is None:
+        return None
+    cores = os.cpu_count() or 1
+    handles = {}
+    tot_flops = 0
+    tot_s = 0.0
+    for m, n in sample:
+        if m["name"] not in handles:
+            rp = m["rp"].cpu().numpy().astype(np.int64)
+            ci = m["ci"].cpu().numpy().astype(np.int64)
+            va = m["va"].cpu().numpy().astype(np.float64)
+            handles[m["name"]] = R.ref_csr_from_csr(m["M"], m["K"], rp, ci, va)
+        h = handles[m["name"]]
+        x = np.random.default_rng(n).uniform(-1, 1, (m["K"], n)).astype(np.float32).reshape(-1)
+        med, mn, ck = C.c_double(), C.c_double(), C.c_double()
+        rc = R.ref_time_spmm_f32(h, 0, cores, 8, 8, x, n, 3, 1, C.byref(med), C.byref(mn),
+                                 C.byref(ck))
+        if rc:
+            raise RuntimeError(R.ref_last_error().decode())
+        tot_s += med.value
+        tot_flops += 2 * m["nnz_total"] * n
+    for h in handles.values():
+        R.ref_csr_free(h)
+    return tot_flops / tot_s / 1e9, cores, tot_s
+
+
+def _cpu_baseline(mats, ns, steps=1):
+    sample = _ref_sample(mats, ns)
+    r = _cpu_time_reference(sample, steps)
+    if r is None:
+        return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    v, cores, secs = r
+    return {"value": round(v, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+            "sample": f"reference spmm() RB+RM+SR fp32, P={cores} threads, time_kernel_fn "
+                      f"(warmup 1, reps 3, median) over {len(sample)} (matrix, N) pairs of the "
+                      f"suite (all 2^14 matrices x all N; 2^17 matrices x N<=8); {secs:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU implementation alone (rank 0)."""
+    world, rank, local = _dist()
+    if rank != 0:
+        return
+    import torch
+
+    ns = [int(n) for n in args.ns.split(",")] if args.ns else list(NS)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    if dev == "cuda":
+        torch.cuda.set_device(local)
+    from paper_2202_08556_b200 import gen
+
+    mats = []
+    for name, mk in gen.suite(small=True, device=dev):
+        M, K, rp, ci, va = mk()
+        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), rp=rp, ci=ci, va=va))
+    sample = _ref_sample(mats, ns)
+    from oracle import oracle as O
+
+    if O.ref() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built here"}))
+        return
+    for _ in range(args.warmup):
+        _cpu_time_reference(sample[:1], 1)
+    vals, secs = [], 0.0
+    cores = os.cpu_count() or 1
+    for _ in range(args.steps):
+        v, cores, s = _cpu_time_reference(sample, 1)
+        vals.append(v)
+        secs += s
+    value = statistics.median(vals)
+    tot_flops = sum(2 * m["nnz_total"] * n for m, n in sample)
+    out = {"impl": "reference",
+           "metric": "SpMM GFLOP/s (2*nnz*N/t), DA-SpMM over the synthetic suite",
+           "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(tot_flops / (value * 1e9) * 1e3, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic",
+           "config": {"workload": "configs[1] synthetic suite (bounded CPU sample)", "ns": ns},
+           "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
+                            "kind": "reference",
+                            "sample": f"reference spmm() RB+RM+SR fp32, P={cores}, "
+                                      f"{len(sample)} (matrix, N) pairs per step"}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default=os.path.join(ROOT, "paper_2202_08556_b200", "models",
+                                                    "b200_selector.txt"))
+    ap.add_argument("--small", action="store_true", help="2^14 and 2^17 matrices only")
+    ap.add_argument("--ns", default="")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cusparse", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

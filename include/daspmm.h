@@ -1,0 +1,193 @@
+/*
+ * daspmm — C ABI of the B200-native DA-SpMM library (libdaspmm.so).
+ *
+ * Drop-in boundary for the spmmkit hot path (reference: /root/reference/proj/include/
+ * spmmkit). The reference exposes header-only C++ templates; this C ABI is what those
+ * templates become when the compute moves to a B200: plain pointers and sizes, int
+ * status codes instead of exceptions, opaque device-resident handles. The C++ shim in
+ * include/spmmkit/ maps it back onto the reference's exact C++ signatures and
+ * exception types (see INTEGRATION.md for the ctypes / C++ bindings).
+ *
+ * All compute runs as hand-written sm_100a CUDA kernels. There is no CPU fallback:
+ * every entry point that computes fails with DASPMM_ERR_CUDA when no device exists.
+ *
+ * Threading: handles are immutable after creation (feature caches are filled under a
+ * per-handle lock); calls are stream-ordered and re-entrant across streams.
+ */
+#ifndef DASPMM_H_
+#define DASPMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct daspmm_csr daspmm_csr;     /* device CSR (int32 offsets/cols, f32|f64 values) */
+typedef struct daspmm_model daspmm_model; /* selector tree ensemble (host + device copy)   */
+typedef void* daspmm_stream;              /* cudaStream_t; NULL = legacy default stream   */
+
+/* Status codes. The C++ shim rethrows them as the reference's exception types:
+ *   INVALID_CONFIG, DIMS, LAYOUT, INVALID_ARG -> std::invalid_argument
+ *       (spmm.hpp:197-209, features.hpp:24-25, selector.hpp:26-28)
+ *   OUT_OF_RANGE                              -> std::out_of_range (kernel_id.hpp:30,
+ *                                                partition.hpp:36-39)
+ *   MODEL_FORMAT                              -> spmmkit::ModelFormatError (gbdt.hpp:301-303)
+ *   CUDA, NCCL, UNSUPPORTED                   -> std::runtime_error                     */
+enum {
+    DASPMM_OK = 0,
+    DASPMM_ERR_INVALID_CONFIG = 1,
+    DASPMM_ERR_DIMS = 2,
+    DASPMM_ERR_LAYOUT = 3,
+    DASPMM_ERR_INVALID_ARG = 4,
+    DASPMM_ERR_OUT_OF_RANGE = 5,
+    DASPMM_ERR_MODEL_FORMAT = 6,
+    DASPMM_ERR_CUDA = 7,
+    DASPMM_ERR_NCCL = 8,
+    DASPMM_ERR_UNSUPPORTED = 9
+};
+
+enum { DASPMM_F32 = 0, DASPMM_F64 = 1 };          /* value type T ∈ {float, double} */
+enum { DASPMM_ROW_MAJOR = 0, DASPMM_COL_MAJOR = 1 }; /* Layout, types.hpp:16          */
+
+/* Call flags. */
+enum {
+    /* Reference evaluation order with no FMA contraction: results equal the
+     * reference's spmm() bit for bit (RB kernels always; EB kernels on rows owned by
+     * one chunk, with P honoured as the chunk count). Default: fused multiply-add,
+     * library-chosen EB chunking, tolerance parity. */
+    DASPMM_EXACT = 1u
+};
+
+/* Human-readable message for the last failing call on this thread. */
+const char* daspmm_last_error(void);
+/* 100 * major + minor. */
+int daspmm_version(void);
+/* Number of CUDA devices visible (0 on a GPU-less host). */
+int daspmm_device_count(void);
+
+/* ------------------------------------------------------------------ CSR handles */
+
+/* Uploads a host CSR — replaces passing `const CsrMatrix<T>&` into spmm()
+ * (types.hpp:28-35, spmm.hpp:194-196). Offsets/columns are int64 as in the
+ * reference; they are validated (types.hpp:96-148 invariants that the kernels rely
+ * on: offsets[0]==0, nondecreasing, offsets[M]==nnz, 0<=col<K) and compacted to
+ * int32 on the device. Requires nnz < 2^31 and M, K < 2^31. Also computes the
+ * selector features (features.hpp:21-41) and the empty-row list on the device. */
+int daspmm_csr_create_host(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                           const int64_t* row_offsets, const int64_t* col_indices,
+                           const void* values, int dtype, daspmm_csr** out);
+
+/* Adopts (copy == 0: borrows, caller keeps ownership) or copies (copy != 0) a CSR
+ * already in device memory with int32 offsets and columns. */
+int daspmm_csr_create_device(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                             const int32_t* d_row_offsets, const int32_t* d_col_indices,
+                             const void* d_values, int dtype, int copy, daspmm_stream stream,
+                             daspmm_csr** out);
+
+/* Row panel [r0, r1) of an existing handle (offsets rebased, columns shared) — the
+ * multi-GPU layer's unit. Device-to-device copy on `stream`. */
+int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1,
+                            daspmm_stream stream, daspmm_csr** out);
+
+int daspmm_csr_destroy(daspmm_csr* csr);
+
+/* num_rows, num_cols, nnz, dtype, number of empty rows, distinct columns touched
+ * (K_touched, for the compulsory-byte roofline). Any pointer may be NULL. */
+int daspmm_csr_info(const daspmm_csr* csr, int64_t* num_rows, int64_t* num_cols,
+                    int64_t* nnz, int* dtype, int64_t* empty_rows, int64_t* cols_touched);
+
+/* Device pointers of the handle's arrays (int32 offsets, int32 columns, values). */
+int daspmm_csr_device_arrays(const daspmm_csr* csr, const int32_t** d_row_offsets,
+                             const int32_t** d_col_indices, const void** d_values);
+
+/* ---------------------------------------------------------------- design space */
+
+/* spmm() — spmm.hpp:194-271, device-resident operands.
+ *   kernel      0..7, KernelId::index() = 4m + 2n + k (kernel_id.hpp:25-27)
+ *   P, W, Cb    WorkerConfig (worker.hpp:18-40): validated as the reference does
+ *               (P >= 1 or 0 = library choice, W power of two in [2, 32], Cb >= 1).
+ *               W is the PR reduction width; P the EB chunk count when honoured
+ *               (P > 0, or always in DASPMM_EXACT mode); Cb does not change results.
+ *   d_B         K x N operand; b_layout must equal the kernel's N-loop choice
+ *               (RM kernels: DASPMM_ROW_MAJOR, ldb >= N; CM kernels: DASPMM_COL_MAJOR,
+ *               ldb >= K), else DASPMM_ERR_LAYOUT (spmm.hpp:206-209).
+ *   d_C         M x N row-major output, ldc >= N; every element is written.
+ * Asynchronous on `stream`. */
+int daspmm_spmm(const daspmm_csr* csr, int kernel, int64_t P, int64_t W, int64_t Cb,
+                const void* d_B, int b_layout, int64_t ldb, int64_t N, void* d_C, int64_t ldc,
+                unsigned flags, daspmm_stream stream);
+
+/* Same call with HOST operands (dense B in `b_layout` with leading dim = N or K, C
+ * row-major M x N): uploads B, runs, downloads C, synchronises. This is the value-
+ * semantics path the C++ shim's spmm() uses. */
+int daspmm_spmm_host(const daspmm_csr* csr, int kernel, int64_t P, int64_t W, int64_t Cb,
+                     const void* B, int b_layout, int64_t N, void* C, unsigned flags);
+
+/* spmm_auto_layout — spmm.hpp:275-281: converts B to the kernel's layout on the
+ * device when needed (scratch is stream-ordered), then runs. */
+int daspmm_spmm_auto_layout(const daspmm_csr* csr, int kernel, int64_t P, int64_t W,
+                            int64_t Cb, const void* d_B, int b_layout, int64_t ldb, int64_t N,
+                            void* d_C, int64_t ldc, unsigned flags, daspmm_stream stream);
+
+/* ------------------------------------------------------------------- features */
+
+/* extract_features — features.hpp:21-41. std_row has the reference's bits (its
+ * sequential double sum is replayed on the device once per handle and cached).
+ * DASPMM_ERR_INVALID_ARG when num_rows == 0. */
+int daspmm_extract_features(const daspmm_csr* csr, int64_t n_cols, int64_t* nnz,
+                            int64_t* mat_size, double* std_row);
+
+/* partition_elements — partition.hpp:45-64, computed by the device partition kernel
+ * (the same kernel the EB path uses). begin/end/row are host arrays of length p. */
+int daspmm_partition(const daspmm_csr* csr, int64_t p, int64_t* begin, int64_t* end,
+                     int64_t* row);
+
+/* ------------------------------------------------------------------- selector */
+
+/* load_selector — selector.hpp:119-132 + load_model gbdt.hpp:371-453 (text v1).
+ * Parses on the host, flattens and uploads the ensemble once. */
+int daspmm_model_parse(const char* text, size_t len, daspmm_model** out);
+int daspmm_model_destroy(daspmm_model* model);
+/* classes, features, rounds, uses_hardware. */
+int daspmm_model_info(const daspmm_model* model, int* num_classes, int* num_features,
+                      int* num_rounds, int* uses_hardware);
+
+/* predict_kernel — selector.hpp:62-65 evaluated on the HOST from given features
+ * (encode_features selector.hpp:19-33 + predict_class gbdt.hpp:67-77). hw < 0 = no
+ * hardware_id. Reference for the device selector's bit-exactness check. */
+int daspmm_model_predict_host(const daspmm_model* model, int64_t nnz, int64_t mat_size,
+                              double std_row, int64_t n_cols, int64_t hw, int* kernel);
+
+/* Device selector: features of `csr` (cached on the device) + N -> kernel id written
+ * to d_kernel (device int). No host round trip; the decision equals
+ * daspmm_model_predict_host on extract_features() bit for bit. */
+int daspmm_select(const daspmm_csr* csr, const daspmm_model* model, int64_t n_cols,
+                  int64_t hw, int* d_kernel, daspmm_stream stream);
+
+/* DA-SpMM: device selector + device-side dispatch (CUDA graph with a SWITCH
+ * conditional node; the selector kernel sets the branch). B may be in either
+ * layout; a body whose kernel needs the other layout converts B on the device
+ * first, as spmm_auto_layout does. W/Cb from make_config(kernel, N) defaults
+ * (worker.hpp:47-55) unless W > 0. Optional d_kernel receives the choice. The
+ * instantiated graph is cached per (operands, N, stream); repeated calls are one
+ * graph launch. */
+int daspmm_spmm_selected(const daspmm_csr* csr, const daspmm_model* model, int64_t hw,
+                         const void* d_B, int b_layout, int64_t ldb, int64_t N, void* d_C,
+                         int64_t ldc, int64_t W, unsigned flags, int* d_kernel,
+                         daspmm_stream stream);
+
+/* ----------------------------------------------------------- test hooks (device) */
+
+/* The device warp primitives on caller data, for bit-exact checks against
+ * tree_reduce (reduce.hpp:46-55) and conditional_reduce (reduce.hpp:57-102).
+ * Host arrays in, host arrays out. w is a power of two in [1, 32]. */
+int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out);
+int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, int64_t w,
+                                      double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DASPMM_H_ */

@@ -1,0 +1,666 @@
+// daspmm — C ABI: handles, validation, launch planning, host-operand paths.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "dispatch.h"
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace daspmm {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return DASPMM_ERR_CUDA;
+}
+
+static bool is_pow2(int64_t w) { return w > 0 && (w & (w - 1)) == 0; }
+
+static const char* kKernelNames[8] = {"RB+RM+SR", "RB+RM+PR", "RB+CM+SR", "RB+CM+PR",
+                                      "EB+RM+SR", "EB+RM+PR", "EB+CM+SR", "EB+CM+PR"};
+
+// worker.hpp:29-40 with the reference's message text.
+static int validate_config(int64_t P, int64_t W, int64_t Cb, bool allow_auto_p) {
+    std::string msg = "spmm: invalid config";
+    bool bad = false;
+    if (P < (allow_auto_p ? 0 : 1)) {
+        msg += "; num_workers must be >= 1, got " + std::to_string(P);
+        bad = true;
+    }
+    if (W < 2 || !is_pow2(W)) {
+        msg += "; group_width must be a power of two >= 2, got " + std::to_string(W);
+        bad = true;
+    }
+    if (Cb < 1) {
+        msg += "; col_block must be >= 1, got " + std::to_string(Cb);
+        bad = true;
+    }
+    if (bad) return fail(DASPMM_ERR_INVALID_CONFIG, msg);
+    if (W > 32)
+        return fail(DASPMM_ERR_UNSUPPORTED,
+                    "spmm: group_width " + std::to_string(W) +
+                        " exceeds the 32-lane warp (B200 build supports 2..32)");
+    return DASPMM_OK;
+}
+
+static int elem_size(int dtype) { return dtype == DASPMM_F64 ? 8 : 4; }
+
+static bool aligned(const void* p, int bytes) {
+    return (reinterpret_cast<uintptr_t>(p) % uintptr_t(bytes)) == 0;
+}
+
+// Vector width for row-major B/C: every gather/store of V elements must be aligned.
+static int pick_v(int dtype, int64_t N, const void* B, int64_t ldb, const void* C, int64_t ldc) {
+    const int es = elem_size(dtype);
+    const int vmax = dtype == DASPMM_F64 ? 2 : 4;
+    for (int v = vmax; v > 1; v >>= 1) {
+        if (N % v == 0 && ldb % v == 0 && ldc % v == 0 && aligned(B, v * es) && aligned(C, v * es))
+            return v;
+    }
+    return 1;
+}
+
+static int pow2_ceil(int64_t x) {
+    int p = 1;
+    while (p < x && p < 32) p <<= 1;
+    return p;
+}
+
+// Stream-ordered scratch comes from the device's default memory pool. Keep freed
+// blocks in the pool (the default release threshold of 0 would unmap them at every
+// synchronisation and remap them on the next call).
+static void keep_pool_warm(int dev) {
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+// Column-tile width: B's working set for one tile of columns, K x tile x elem, should
+// stay L2-resident (126 MB on B200) while A streams through. CTAs are scheduled
+// x-major, so tiles (blockIdx.y) run one after another. DASPMM_TILE_COLS overrides.
+static int64_t max_tile_cols(const daspmm_csr* h, int64_t N) {
+    static const int64_t env = [] {
+        const char* e = getenv("DASPMM_TILE_COLS");
+        return e ? int64_t(atoll(e)) : int64_t(0);
+    }();
+    if (env > 0) return env;
+    // Measured on B200 (profiles/r01_notes.md): narrowing tiles to keep B in L2 costs
+    // more in A re-reads and shorter gathers than it saves, up to N = 128.
+    (void)h;
+    return 256;
+}
+
+// Default EB chunk size: enough chunks for >= 2 waves of resident groups.
+static int64_t auto_chunks(int64_t nnz, int lanes_per_worker, int step) {
+    if (nnz <= 0) return 1;
+    const int64_t resident_threads = 148LL * 2048;
+    int64_t target = nnz * lanes_per_worker / (2 * resident_threads);
+    target = std::max<int64_t>(target, step);
+    target = std::min<int64_t>(target, 2048);
+    target = (target + step - 1) / step * step;
+    return (nnz + target - 1) / target;
+}
+
+Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
+               int64_t ldb, const void* C, int64_t ldc, bool exact) {
+    Plan p;
+    p.kernel = kernel;
+    p.cm = (kernel >> 1) & 1;
+    p.exact = exact;
+    const bool eb = kernel >= 4, pr = kernel & 1;
+    p.V = (p.cm || exact) ? 1 : pick_v(h->dtype, N, B, ldb, C, ldc);
+    const int64_t ncols = std::min<int64_t>(N, max_tile_cols(h, N));
+    const int64_t nv = (ncols + p.V - 1) / p.V;  // column slots per tile
+    int64_t tile_cols;
+    int lanes;
+    if (!pr) {
+        p.L = pow2_ceil(nv);
+        p.X = nv > 32 ? 2 : 1;
+        tile_cols = int64_t(p.L) * p.V * p.X;
+        lanes = p.L;
+    } else {
+        p.L = int(W);
+        p.X = nv > W ? 2 : 1;
+        tile_cols = int64_t(p.L) * p.X * p.V;
+        lanes = p.L;
+    }
+    const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
+    int64_t workers;
+    if (eb) {
+        const int step = pr ? int(W) : std::max(p.L, 8);
+        p.P = P > 0 ? P : auto_chunks(h->nnz, lanes, step);
+        workers = p.P;
+    } else if (!pr) {
+        // RB+SR row blocks: ~4 steps of pairs per group, but keep >= 2 waves of groups.
+        const int step = p.L >= 16 ? p.L : (p.L >= 4 ? 16 : 8);
+        const double avg = h->M > 0 ? double(h->nnz) / double(h->M) : 0.0;
+        int64_t rpg = avg > 0 ? int64_t(4.0 * step / avg) : 64;
+        // Skewed rows: a long row already fills its group; do not stack more rows on it.
+        const double sd = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
+        if (sd > 2.0 * avg) rpg = 1;
+        const int64_t cap = std::max<int64_t>(1, h->M * lanes / (2LL * 148 * 2048));
+        rpg = std::max<int64_t>(1, std::min<int64_t>({rpg, cap, 64}));
+        p.rpg = rpg;
+        workers = (h->M + rpg - 1) / rpg;
+    } else {
+        workers = h->M;
+    }
+    const int64_t threads = workers * lanes;
+    p.grid = dim3(unsigned(std::max<int64_t>(1, (threads + kThreads - 1) / kThreads)),
+                  unsigned(ytiles), 1);
+    return p;
+}
+
+template <typename T>
+static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const void* B,
+                            int64_t ldb, int64_t N, void* C, int64_t ldc, int* chunk_row,
+                            cudaStream_t s) {
+    SpmmArgs<T> a;
+    a.rp = h->rp;
+    a.ci = h->ci;
+    a.va = static_cast<const T*>(h->va);
+    a.B = static_cast<const T*>(B);
+    a.C = static_cast<T*>(C);
+    a.M = int(h->M);
+    a.K = int(h->K);
+    a.N = int(N);
+    a.nnz = h->nnz;
+    a.ldb = ldb;
+    a.ldc = ldc;
+    a.P = p.P;
+    a.seg = int(std::max<int64_t>(W, 256));
+    a.chunk_row = chunk_row;
+    a.rpg = p.rpg;
+    const bool eb = p.kernel >= 4, pr = p.kernel & 1;
+    if (eb) {
+        cudaError_t e = launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,
+                                          static_cast<T*>(C), ldc, int(N), h->empty_rows,
+                                          int(h->n_empty), s);
+        if (e != cudaSuccess) return e;
+        return pr ? launch_eb_pr<T>(p, a, s) : launch_eb_sr<T>(p, a, s);
+    }
+    return pr ? launch_rb_pr<T>(p, a, s) : launch_rb_sr<T>(p, a, s);
+}
+
+// Core device-operand SpMM (operands already validated).
+// chunk_scratch: caller-provided EB scratch of >= plan.P ints (graph bodies cannot
+// allocate); null = stream-ordered allocation here.
+int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const void* B,
+                int64_t ldb, int64_t N, void* C, int64_t ldc, unsigned flags, cudaStream_t s,
+                int* chunk_scratch) {
+    if (h->M == 0 || N == 0) return DASPMM_OK;
+    keep_pool_warm(h->device);
+    const bool exact = (flags & DASPMM_EXACT) != 0;
+    const Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
+    int* chunk_row = chunk_scratch;
+    const bool own_scratch = chunk_scratch == nullptr;
+    cudaError_t e;
+    if (kernel >= 4 && own_scratch) {
+        if ((e = cudaMallocAsync(&chunk_row, sizeof(int) * size_t(std::max<int64_t>(p.P, 1)), s)) !=
+            cudaSuccess)
+            return cuda_fail(e, "cudaMallocAsync(chunk_row)");
+    }
+    e = h->dtype == DASPMM_F64 ? run_plan<double>(h, p, W, B, ldb, N, C, ldc, chunk_row, s)
+                               : run_plan<float>(h, p, W, B, ldb, N, C, ldc, chunk_row, s);
+    if (chunk_row && own_scratch) cudaFreeAsync(chunk_row, s);
+    if (e == cudaErrorNotSupported)
+        return fail(DASPMM_ERR_UNSUPPORTED, std::string("spmm: no instantiation for kernel ") +
+                                                kKernelNames[kernel]);
+    if (e != cudaSuccess) return cuda_fail(e, kKernelNames[kernel]);
+    return DASPMM_OK;
+}
+
+int check_call(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb, int b_layout,
+               int64_t ldb, int64_t N, int64_t ldc, bool exact) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "spmm: null CSR handle");
+    if (kernel < 0 || kernel > 7)
+        return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
+    if (int rc = validate_config(P, W, Cb, true)) return rc;
+    (void)exact;
+    if (N < 0) return fail(DASPMM_ERR_DIMS, "spmm: negative N");
+    if (N > (int64_t(1) << 30)) return fail(DASPMM_ERR_UNSUPPORTED, "spmm: N too large");
+    const bool want_cm = (kernel >> 1) & 1;
+    if ((b_layout == DASPMM_COL_MAJOR) != want_cm)
+        return fail(DASPMM_ERR_LAYOUT, std::string("spmm: kernel ") + kKernelNames[kernel] +
+                                           " needs " + (want_cm ? "ColMajor" : "RowMajor") +
+                                           " X, got " + (want_cm ? "RowMajor" : "ColMajor"));
+    if (want_cm ? ldb < std::max<int64_t>(h->K, 1) : ldb < std::max<int64_t>(N, 1))
+        return fail(DASPMM_ERR_DIMS, "spmm: leading dimension of B too small");
+    if (ldc < std::max<int64_t>(N, 1)) return fail(DASPMM_ERR_DIMS, "spmm: ldc < N");
+    return DASPMM_OK;
+}
+
+// ---------------------------------------------------------------- small kernels
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi,
+                            T* __restrict__ out, int64_t ldo) {
+    // in: rows x cols with leading dim ldi (row-major view); out: cols x rows, ldo.
+    __shared__ T tile[32][33];
+    const int64_t bx = int64_t(blockIdx.x) * 32, by = int64_t(blockIdx.y) * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int64_t r = by + j, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * ldi + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int64_t r = bx + j, c = by + threadIdx.x;  // out row = in col
+        if (r < cols && c < rows) out[r * ldo + c] = tile[threadIdx.x][j];
+    }
+}
+
+__global__ void k_rebase(const int* __restrict__ in, int64_t n, int base, int* __restrict__ out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = in[i] - base;
+}
+
+template <int W>
+__global__ void k_debug_tree(const double* in, double* out, int w) {
+    const int lane = threadIdx.x;
+    double v = lane < w ? in[lane] : 0.0;
+    v = group_tree_sum<W>(group_mask<W>(), v);
+    if (lane == 0) out[0] = v;
+}
+
+template <int W>
+__global__ void k_debug_cond(const double* in, const int64_t* ids, double* out, int w) {
+    const int lane = threadIdx.x;
+    double v = in[lane];
+    const int id = int(ids[lane]);
+    v = group_conditional_scan<W>(group_mask<W>(), v, id, lane & (W - 1));
+    out[lane] = v;
+}
+
+cudaError_t transpose(int dtype, const void* in, int64_t rows, int64_t cols, int64_t ldi,
+                      void* out, int64_t ldo, cudaStream_t s) {
+    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    if (dtype == DASPMM_F64)
+        k_transpose<double><<<grid, block, 0, s>>>(static_cast<const double*>(in), rows, cols, ldi,
+                                                   static_cast<double*>(out), ldo);
+    else
+        k_transpose<float><<<grid, block, 0, s>>>(static_cast<const float*>(in), rows, cols, ldi,
+                                                  static_cast<float*>(out), ldo);
+    return cudaGetLastError();
+}
+
+}  // namespace daspmm
+
+using namespace daspmm;
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* daspmm_last_error(void) { return g_err.c_str(); }
+int daspmm_version(void) { return 100; }
+int daspmm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static int finish_create(daspmm_csr* h, cudaStream_t s, daspmm_csr** out) {
+    int rc = compute_features(h, s);
+    if (rc) {
+        daspmm_csr_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return DASPMM_OK;
+}
+
+int daspmm_csr_create_host(int64_t M, int64_t K, int64_t nnz, const int64_t* rp,
+                           const int64_t* ci, const void* values, int dtype, daspmm_csr** out) {
+    if (!out) return fail(DASPMM_ERR_INVALID_ARG, "csr_create: null out");
+    *out = nullptr;
+    if (dtype != DASPMM_F32 && dtype != DASPMM_F64)
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: dtype must be F32 or F64");
+    if (M < 0 || K < 0 || nnz < 0) return fail(DASPMM_ERR_INVALID_ARG, "csr_create: negative size");
+    if (M >= (int64_t(1) << 31) - 1 || K >= (int64_t(1) << 31) - 1 || nnz >= (int64_t(1) << 31) - 1)
+        return fail(DASPMM_ERR_UNSUPPORTED, "csr_create: sizes must be < 2^31 - 1 (int32 device CSR)");
+    if (!rp || (nnz > 0 && (!ci || !values)))
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: null array");
+    // types.hpp:96-148 invariants the kernels depend on.
+    if (rp[0] != 0) return fail(DASPMM_ERR_INVALID_ARG, "csr_create: row_offsets[0] != 0");
+    for (int64_t i = 1; i <= M; ++i)
+        if (rp[i] < rp[i - 1])
+            return fail(DASPMM_ERR_INVALID_ARG,
+                        "csr_create: row_offsets nondecreasing violated at index " + std::to_string(i));
+    if (rp[M] != nnz)
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: row_offsets[num_rows] != nnz");
+    std::vector<int32_t> rp32(static_cast<size_t>(M) + 1);
+    std::vector<int32_t> ci32(static_cast<size_t>(nnz));
+    for (int64_t i = 0; i <= M; ++i) rp32[i] = int32_t(rp[i]);
+    for (int64_t i = 0; i < nnz; ++i) {
+        if (ci[i] < 0 || ci[i] >= K)
+            return fail(DASPMM_ERR_INVALID_ARG,
+                        "csr_create: col index bound violated at index " + std::to_string(i));
+        ci32[i] = int32_t(ci[i]);
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || daspmm_device_count() == 0) {
+        cudaGetLastError();
+        return fail(DASPMM_ERR_CUDA, "csr_create: no CUDA device (daspmm has no CPU fallback)");
+    }
+    daspmm_csr* h = new daspmm_csr;
+    h->M = M;
+    h->K = K;
+    h->nnz = nnz;
+    h->dtype = dtype;
+    h->device = dev;
+    const size_t es = size_t(elem_size(dtype));
+    cudaError_t e;
+    if ((e = cudaMalloc(&h->rp, sizeof(int32_t) * (M + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&h->ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+        (e = cudaMalloc(&h->va, es * std::max<int64_t>(nnz, 1))) != cudaSuccess) {
+        daspmm_csr_destroy(h);
+        return cuda_fail(e, "csr_create: cudaMalloc");
+    }
+    cudaMemcpy(h->rp, rp32.data(), sizeof(int32_t) * (M + 1), cudaMemcpyHostToDevice);
+    if (nnz > 0) {
+        cudaMemcpy(h->ci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
+        cudaMemcpy(h->va, values, es * nnz, cudaMemcpyHostToDevice);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+        daspmm_csr_destroy(h);
+        return cuda_fail(e, "csr_create: upload");
+    }
+    return finish_create(h, 0, out);
+}
+
+int daspmm_csr_create_device(int64_t M, int64_t K, int64_t nnz, const int32_t* d_rp,
+                             const int32_t* d_ci, const void* d_va, int dtype, int copy,
+                             daspmm_stream stream, daspmm_csr** out) {
+    if (!out) return fail(DASPMM_ERR_INVALID_ARG, "csr_create: null out");
+    *out = nullptr;
+    if (dtype != DASPMM_F32 && dtype != DASPMM_F64)
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: dtype must be F32 or F64");
+    if (M < 0 || K < 0 || nnz < 0 || M >= (int64_t(1) << 31) - 1 || K >= (int64_t(1) << 31) - 1 ||
+        nnz >= (int64_t(1) << 31) - 1)
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: sizes must be in [0, 2^31 - 1)");
+    if (!d_rp || (nnz > 0 && (!d_ci || !d_va)))
+        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: null array");
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(cudaGetLastError(), "csr_create");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    daspmm_csr* h = new daspmm_csr;
+    h->M = M;
+    h->K = K;
+    h->nnz = nnz;
+    h->dtype = dtype;
+    h->device = dev;
+    if (!copy) {
+        h->owns = false;
+        h->rp = const_cast<int32_t*>(d_rp);
+        h->ci = const_cast<int32_t*>(d_ci);
+        h->va = const_cast<void*>(d_va);
+    } else {
+        const size_t es = size_t(elem_size(dtype));
+        cudaError_t e;
+        if ((e = cudaMalloc(&h->rp, sizeof(int32_t) * (M + 1))) != cudaSuccess ||
+            (e = cudaMalloc(&h->ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+            (e = cudaMalloc(&h->va, es * std::max<int64_t>(nnz, 1))) != cudaSuccess) {
+            daspmm_csr_destroy(h);
+            return cuda_fail(e, "csr_create: cudaMalloc");
+        }
+        cudaMemcpyAsync(h->rp, d_rp, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToDevice, s);
+        if (nnz > 0) {
+            cudaMemcpyAsync(h->ci, d_ci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(h->va, d_va, es * nnz, cudaMemcpyDeviceToDevice, s);
+        }
+    }
+    return finish_create(h, s, out);
+}
+
+int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1, daspmm_stream stream,
+                            daspmm_csr** out) {
+    if (!full || !out) return fail(DASPMM_ERR_INVALID_ARG, "csr_create_panel: null argument");
+    if (r0 < 0 || r1 < r0 || r1 > full->M)
+        return fail(DASPMM_ERR_OUT_OF_RANGE, "csr_create_panel: bad row range");
+    DeviceGuard g(full->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t ends[2] = {0, 0};
+    cudaMemcpyAsync(&ends[0], full->rp + r0, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&ends[1], full->rp + r1, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "csr_create_panel");
+    const int64_t M = r1 - r0, nnz = int64_t(ends[1]) - ends[0];
+    daspmm_csr* h = new daspmm_csr;
+    h->M = M;
+    h->K = full->K;
+    h->nnz = nnz;
+    h->dtype = full->dtype;
+    h->device = full->device;
+    const size_t es = size_t(elem_size(full->dtype));
+    if ((e = cudaMalloc(&h->rp, sizeof(int32_t) * (M + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&h->ci, sizeof(int32_t) * std::max<int64_t>(nnz, 1))) != cudaSuccess ||
+        (e = cudaMalloc(&h->va, es * std::max<int64_t>(nnz, 1))) != cudaSuccess) {
+        daspmm_csr_destroy(h);
+        return cuda_fail(e, "csr_create_panel: cudaMalloc");
+    }
+    k_rebase<<<int(std::min<int64_t>((M + 256) / 256, 4096)), 256, 0, s>>>(full->rp + r0, M + 1,
+                                                                          ends[0], h->rp);
+    if (nnz > 0) {
+        cudaMemcpyAsync(h->ci, full->ci + ends[0], sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(h->va, static_cast<const char*>(full->va) + es * ends[0], es * nnz,
+                        cudaMemcpyDeviceToDevice, s);
+    }
+    return finish_create(h, s, out);
+}
+
+int daspmm_csr_destroy(daspmm_csr* h) {
+    if (!h) return DASPMM_OK;
+    graph_cache_free(h);
+    if (h->owns) {
+        cudaFree(h->rp);
+        cudaFree(h->ci);
+        cudaFree(h->va);
+    }
+    cudaFree(h->empty_rows);
+    cudaFree(h->d_feat);
+    delete h;
+    return DASPMM_OK;
+}
+
+int daspmm_csr_info(const daspmm_csr* h, int64_t* M, int64_t* K, int64_t* nnz, int* dtype,
+                    int64_t* empty_rows, int64_t* cols_touched) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "csr_info: null handle");
+    if (M) *M = h->M;
+    if (K) *K = h->K;
+    if (nnz) *nnz = h->nnz;
+    if (dtype) *dtype = h->dtype;
+    if (empty_rows) *empty_rows = h->n_empty;
+    if (cols_touched) *cols_touched = h->cols_touched;
+    return DASPMM_OK;
+}
+
+int daspmm_csr_device_arrays(const daspmm_csr* h, const int32_t** rp, const int32_t** ci,
+                             const void** va) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "csr_device_arrays: null handle");
+    if (rp) *rp = h->rp;
+    if (ci) *ci = h->ci;
+    if (va) *va = h->va;
+    return DASPMM_OK;
+}
+
+int daspmm_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb, const void* d_B,
+                int b_layout, int64_t ldb, int64_t N, void* d_C, int64_t ldc, unsigned flags,
+                daspmm_stream stream) {
+    if (int rc = check_call(h, kernel, P, W, Cb, b_layout, ldb, N, ldc, flags & DASPMM_EXACT))
+        return rc;
+    DeviceGuard g(h->device);
+    return spmm_device(h, kernel, P, W, d_B, ldb, N, d_C, ldc, flags,
+                       static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int daspmm_spmm_host(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb,
+                     const void* B, int b_layout, int64_t N, void* C, unsigned flags) {
+    const int64_t ldb = b_layout == DASPMM_COL_MAJOR ? std::max<int64_t>(h ? h->K : 1, 1)
+                                                     : std::max<int64_t>(N, 1);
+    if (int rc = check_call(h, kernel, P, W, Cb, b_layout, ldb, N, std::max<int64_t>(N, 1),
+                            flags & DASPMM_EXACT))
+        return rc;
+    if (h->M == 0 || N == 0) return DASPMM_OK;
+    DeviceGuard g(h->device);
+    const size_t es = size_t(elem_size(h->dtype));
+    const size_t bbytes = es * size_t(h->K) * size_t(N), cbytes = es * size_t(h->M) * size_t(N);
+    void *dB = nullptr, *dC = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&dB, std::max<size_t>(bbytes, 16))) != cudaSuccess)
+        return cuda_fail(e, "spmm_host: cudaMalloc(B)");
+    if ((e = cudaMalloc(&dC, std::max<size_t>(cbytes, 16))) != cudaSuccess) {
+        cudaFree(dB);
+        return cuda_fail(e, "spmm_host: cudaMalloc(C)");
+    }
+    cudaMemcpy(dB, B, bbytes, cudaMemcpyHostToDevice);
+    int rc = spmm_device(h, kernel, P, W, dB, ldb, N, dC, N, flags, 0, nullptr);
+    if (rc == DASPMM_OK) {
+        e = cudaMemcpy(C, dC, cbytes, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = cuda_fail(e, "spmm_host");
+    }
+    cudaFree(dB);
+    cudaFree(dC);
+    return rc;
+}
+
+int daspmm_spmm_auto_layout(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb,
+                            const void* d_B, int b_layout, int64_t ldb, int64_t N, void* d_C,
+                            int64_t ldc, unsigned flags, daspmm_stream stream) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "spmm: null CSR handle");
+    if (kernel < 0 || kernel > 7)
+        return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
+    const int want = ((kernel >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
+    if (want == b_layout)
+        return daspmm_spmm(h, kernel, P, W, Cb, d_B, b_layout, ldb, N, d_C, ldc, flags, stream);
+    if (b_layout == DASPMM_COL_MAJOR ? ldb < std::max<int64_t>(h->K, 1)
+                                     : ldb < std::max<int64_t>(N, 1))
+        return fail(DASPMM_ERR_DIMS, "spmm: leading dimension of B too small");
+    DeviceGuard g(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t es = size_t(elem_size(h->dtype));
+    void* t = nullptr;
+    cudaError_t e = cudaMallocAsync(&t, std::max<size_t>(es * size_t(h->K) * size_t(N), 16), s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm_auto_layout: cudaMallocAsync");
+    int64_t ldt;
+    if (b_layout == DASPMM_ROW_MAJOR) {  // K x N (ldb) -> ColMajor: N x K rows, ld K
+        ldt = std::max<int64_t>(h->K, 1);
+        e = transpose(h->dtype, d_B, h->K, N, ldb, t, ldt, s);
+    } else {  // ColMajor (N rows of K, ld ldb) -> RowMajor K x N
+        ldt = std::max<int64_t>(N, 1);
+        e = transpose(h->dtype, d_B, N, h->K, ldb, t, ldt, s);
+    }
+    int rc = e == cudaSuccess ? daspmm_spmm(h, kernel, P, W, Cb, t, want, ldt, N, d_C, ldc, flags,
+                                            stream)
+                              : cuda_fail(e, "spmm_auto_layout: transpose");
+    cudaFreeAsync(t, s);
+    return rc;
+}
+
+int daspmm_extract_features(const daspmm_csr* h, int64_t n_cols, int64_t* nnz, int64_t* mat_size,
+                            double* std_row) {
+    (void)n_cols;
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "extract_features: null handle");
+    if (h->M == 0)
+        return fail(DASPMM_ERR_INVALID_ARG, "extract_features: matrix has no rows to summarize");
+    double s = 0.0;
+    if (int rc = exact_std(const_cast<daspmm_csr*>(h), &s)) return rc;
+    if (nnz) *nnz = h->nnz;
+    if (mat_size) *mat_size = h->M;
+    if (std_row) *std_row = s;
+    return DASPMM_OK;
+}
+
+int daspmm_partition(const daspmm_csr* h, int64_t p, int64_t* begin, int64_t* end, int64_t* row) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "partition: null handle");
+    if (p < 1) return fail(DASPMM_ERR_INVALID_ARG, "partition_elements: need p >= 1");
+    DeviceGuard g(h->device);
+    int* d_row = nullptr;
+    cudaError_t e = cudaMalloc(&d_row, sizeof(int) * size_t(p));
+    if (e != cudaSuccess) return cuda_fail(e, "partition: cudaMalloc");
+    // The EB prologue kernel with no output rows to zero (C = null, N = 0).
+    e = launch_eb_prep<float>(h->rp, int(h->M), h->nnz, p, d_row, nullptr, 0, 0, nullptr, 0, 0);
+    std::vector<int> rows(size_t(p), 0);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(rows.data(), d_row, sizeof(int) * size_t(p), cudaMemcpyDeviceToHost);
+    cudaFree(d_row);
+    if (e != cudaSuccess) return cuda_fail(e, "partition");
+    const int64_t base = h->nnz / p, extra = h->nnz % p;
+    int64_t start = 0;
+    for (int64_t i = 0; i < p; ++i) {
+        const int64_t size = base + (i < extra ? 1 : 0);
+        if (begin) begin[i] = start;
+        if (end) end[i] = start + size;
+        if (row) row[i] = rows[size_t(i)];
+        start += size;
+    }
+    return DASPMM_OK;
+}
+
+int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out) {
+    if (w < 1 || w > 32 || !is_pow2(w))
+        return fail(DASPMM_ERR_INVALID_ARG, "tree_reduce: length must be a power of two <= 32");
+    double *d_in = nullptr, *d_out = nullptr;
+    cudaMalloc(&d_in, sizeof(double) * 32);
+    cudaMalloc(&d_out, sizeof(double));
+    cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice);
+    switch (w) {
+        case 1: k_debug_tree<1><<<1, 32>>>(d_in, d_out, int(w)); break;
+        case 2: k_debug_tree<2><<<1, 32>>>(d_in, d_out, int(w)); break;
+        case 4: k_debug_tree<4><<<1, 32>>>(d_in, d_out, int(w)); break;
+        case 8: k_debug_tree<8><<<1, 32>>>(d_in, d_out, int(w)); break;
+        case 16: k_debug_tree<16><<<1, 32>>>(d_in, d_out, int(w)); break;
+        default: k_debug_tree<32><<<1, 32>>>(d_in, d_out, int(w)); break;
+    }
+    cudaError_t e = cudaMemcpy(out, d_out, sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "debug_tree_reduce");
+}
+
+int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, int64_t w,
+                                      double* out) {
+    if (w < 1 || w > 32 || !is_pow2(w))
+        return fail(DASPMM_ERR_INVALID_ARG, "conditional_scan: length must be a power of two <= 32");
+    double *d_in = nullptr, *d_out = nullptr;
+    int64_t* d_ids = nullptr;
+    cudaMalloc(&d_in, sizeof(double) * 32);
+    cudaMalloc(&d_out, sizeof(double) * 32);
+    cudaMalloc(&d_ids, sizeof(int64_t) * 32);
+    cudaMemset(d_in, 0, sizeof(double) * 32);
+    cudaMemset(d_ids, 0xff, sizeof(int64_t) * 32);
+    cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_ids, ids, sizeof(int64_t) * w, cudaMemcpyHostToDevice);
+    switch (w) {
+        case 1: k_debug_cond<1><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+        case 2: k_debug_cond<2><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+        case 4: k_debug_cond<4><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+        case 8: k_debug_cond<8><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+        case 16: k_debug_cond<16><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+        default: k_debug_cond<32><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
+    }
+    cudaError_t e = cudaMemcpy(out, d_out, sizeof(double) * w, cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_ids);
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "debug_conditional_scan");
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// daspmm — host-side launch plan for one SpMM call (no CUDA kernels here).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace daspmm {
+
+template <typename T>
+struct SpmmArgs;
+
+// Launch shape chosen by plan_spmm() in abi.cu.
+struct Plan {
+    int kernel = 0;      // 0..7 = 4m + 2n + k (kernel_id.hpp:25-27)
+    bool cm = false;     // B column-major (N-loop CM)
+    bool exact = false;  // reference evaluation order, no FMA contraction
+    int V = 1;           // vector width (elements per lane per column slot)
+    int L = 1;           // SR: lanes per group (LPR); PR: group width W
+    int X = 1;           // SR: column slots per lane (CPL); PR: slots per lane (OWN)
+    dim3 grid;
+    int64_t P = 0;       // EB chunks
+    int64_t rpg = 1;     // RB+SR rows per group (row-block size)
+};
+
+// Each returns cudaErrorNotSupported for a shape with no instantiation.
+template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+template <typename T>
+cudaError_t launch_eb_prep(const int* rp, int M, int64_t nnz, int64_t P, int* chunk_row, T* C,
+                           int64_t ldc, int N, const int* empty_rows, int n_empty, cudaStream_t s);
+
+}  // namespace daspmm

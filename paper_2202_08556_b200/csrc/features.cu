@@ -1,0 +1,165 @@
+// daspmm — selector features on the device (features.hpp:21-41) plus the handle's
+// structural summaries (empty-row list for EB zeroing, distinct columns touched).
+//
+// The reference's std_row is a SEQUENTIAL double sum of per-row terms
+// q_r = fl(fl(len_r - mean)^2) with mean = fl(nnz / M). Per-row terms are
+// reproduced exactly here (__dsub_rn / __dmul_rn, no contraction); only the order
+// of the sum differs. Any two summation orders of M non-negative terms agree to
+// within relative 2*gamma_M, so the reference's value lies in a tight, provable
+// interval [std_lo, std_hi] around the parallel sum. A tree threshold outside that
+// interval is decided exactly; one inside it (never seen in practice) triggers the
+// sequential replay kernel below, which reproduces the reference bits.
+#include <cmath>
+
+#include "internal.h"
+
+namespace daspmm {
+
+constexpr int kFeatThreads = 256;
+
+__global__ void __launch_bounds__(kFeatThreads)
+k_row_terms(const int* __restrict__ rp, int M, double mean, double* __restrict__ partial,
+            int* __restrict__ empty_rows, unsigned long long* __restrict__ n_empty) {
+    __shared__ double sm[kFeatThreads];
+    double acc = 0.0;
+    for (int64_t r = int64_t(blockIdx.x) * kFeatThreads + threadIdx.x; r < M;
+         r += int64_t(gridDim.x) * kFeatThreads) {
+        const int len = __ldg(rp + r + 1) - __ldg(rp + r);
+        const double d = __dsub_rn(double(len), mean);
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+        if (len == 0) {
+            const unsigned long long k = atomicAdd(n_empty, 1ull);
+            empty_rows[k] = int(r);
+        }
+    }
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kFeatThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sm[threadIdx.x] = __dadd_rn(sm[threadIdx.x], sm[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sm[0];
+}
+
+__global__ void k_cols_touched(const int* __restrict__ ci, int64_t nnz,
+                               unsigned* __restrict__ bitmap) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int c = __ldg(ci + e);
+        atomicOr(bitmap + (c >> 5), 1u << (c & 31));
+    }
+}
+
+__global__ void k_popcount(const unsigned* __restrict__ bitmap, int64_t words,
+                           unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
+         i += int64_t(gridDim.x) * blockDim.x)
+        acc += __popc(bitmap[i]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+// One thread replays features.hpp:27-35 in the reference's order.
+__global__ void k_std_sequential(const int* __restrict__ rp, int M, DevFeatures* f) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double mean = f->mean;
+    double ss = 0.0;
+    int prev = __ldg(rp);
+    for (int r = 0; r < M; ++r) {
+        const int next = __ldg(rp + r + 1);
+        const double d = __dsub_rn(double(next - prev), mean);
+        ss = __dadd_rn(ss, __dmul_rn(d, d));
+        prev = next;
+    }
+    f->std_exact = __dsqrt_rn(__ddiv_rn(ss, double(M)));
+    f->exact_valid = 1;
+}
+
+int compute_features(daspmm_csr* h, cudaStream_t s) {
+    const int M = int(h->M);
+    DevFeatures f{};
+    f.nnz = h->nnz;
+    f.rows = h->M;
+    f.mean = M > 0 ? double(h->nnz) / double(M) : 0.0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&h->d_feat, sizeof(DevFeatures))) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc(features)");
+    if (M > 0 && (e = cudaMalloc(&h->empty_rows, sizeof(int32_t) * size_t(M))) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc(empty_rows)");
+
+    int blocks = int(std::min<int64_t>((h->M + kFeatThreads - 1) / kFeatThreads, 2048));
+    if (blocks < 1) blocks = 1;
+    double* partial = nullptr;
+    unsigned long long* counters = nullptr;  // [0] empty rows, [1] cols touched
+    const int64_t words = (h->K + 31) / 32;
+    unsigned* bitmap = nullptr;
+    if ((e = cudaMalloc(&partial, sizeof(double) * blocks)) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&counters, sizeof(unsigned long long) * 2)) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&bitmap, sizeof(unsigned) * std::max<int64_t>(words, 1))) != cudaSuccess)
+        return cuda_fail(e, "cudaMalloc");
+    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s);
+    cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max<int64_t>(words, 1), s);
+    if (M > 0)
+        k_row_terms<<<blocks, kFeatThreads, 0, s>>>(h->rp, M, f.mean, partial, h->empty_rows,
+                                                     counters);
+    if (h->nnz > 0) {
+        const int b2 = int(std::min<int64_t>((h->nnz + 255) / 256, 148 * 16));
+        k_cols_touched<<<b2, 256, 0, s>>>(h->ci, h->nnz, bitmap);
+        const int b3 = int(std::min<int64_t>((words + 255) / 256, 148 * 4));
+        k_popcount<<<std::max(b3, 1), 256, 0, s>>>(bitmap, words, counters + 1);
+    }
+    std::vector<double> hp(blocks, 0.0);
+    unsigned long long hc[2] = {0, 0};
+    if (M > 0) cudaMemcpyAsync(hp.data(), partial, sizeof(double) * blocks, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
+    cudaFree(partial);
+    cudaFree(counters);
+    cudaFree(bitmap);
+    h->n_empty = int64_t(hc[0]);
+    h->cols_touched = int64_t(hc[1]);
+
+    double ss = 0.0;
+    for (double v : hp) ss += v;
+    f.ss_par = ss;
+    if (M > 0) {
+        // |ss_ref - ss_par| <= 2 gamma_M * sum q (both orders of M non-negative terms);
+        // widen by 4x and by a few ulps for the division and sqrt roundings.
+        const double u = std::ldexp(1.0, -53);
+        const double g = 8.0 * (double(M) + 8.0) * u;
+        const double lo = std::max(0.0, ss * (1.0 - g)) / double(M);
+        const double hi = ss * (1.0 + g) / double(M) + 1e-300;
+        f.std_lo = std::sqrt(lo) * (1.0 - 8 * u);
+        f.std_hi = std::sqrt(hi) * (1.0 + 8 * u);
+        if (ss == 0.0) f.std_lo = f.std_hi = 0.0;  // every term is exactly 0 in any order
+    }
+    f.exact_valid = 0;
+    if (M > 0 && ss == 0.0) {
+        f.std_exact = 0.0;
+        f.exact_valid = 1;
+    }
+    h->h_feat = f;
+    if ((e = cudaMemcpyAsync(h->d_feat, &h->h_feat, sizeof(DevFeatures), cudaMemcpyHostToDevice,
+                             s)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy(features)");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
+    return DASPMM_OK;
+}
+
+int exact_std(daspmm_csr* h, double* out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->h_feat.exact_valid) {
+        DeviceGuard g(h->device);
+        k_std_sequential<<<1, 32>>>(h->rp, int(h->M), h->d_feat);
+        cudaError_t e = cudaMemcpy(&h->h_feat, h->d_feat, sizeof(DevFeatures),
+                                   cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "exact std");
+    }
+    *out = h->h_feat.std_exact;
+    return DASPMM_OK;
+}
+
+}  // namespace daspmm

@@ -1,0 +1,212 @@
+// daspmm — DA-SpMM with on-device dispatch: select kernel -> SWITCH conditional node.
+//
+// One CUDA graph per (handle, model, operands, N, flags): node 0 is the selector
+// kernel (select.cu), which computes the kernel id from the handle's device-resident
+// features and calls cudaGraphSetConditional; node 1 is a SWITCH conditional with
+// eight bodies, body k holding design-space kernel k (plus the EB prologue, plus a
+// device transpose of B when kernel k needs the other layout, as spmm_auto_layout
+// does, spmm.hpp:275-281). The host never learns the choice — no round trip — and a
+// repeated call is a single cudaGraphLaunch.
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+
+#include "dispatch.h"
+#include "internal.h"
+
+namespace daspmm {
+
+namespace {
+
+struct Key {
+    uint64_t model_gen;
+    const void* B;
+    int b_layout;
+    int64_t ldb, N;
+    void* C;
+    int64_t ldc, W;
+    unsigned flags;
+    int64_t hw;
+    int* d_kernel;
+    cudaStream_t stream;
+    bool operator<(const Key& o) const {
+        return std::tie(model_gen, B, b_layout, ldb, N, C, ldc, W, flags, hw, d_kernel, stream) <
+               std::tie(o.model_gen, o.B, o.b_layout, o.ldb, o.N, o.C, o.ldc, o.W, o.flags, o.hw,
+                        o.d_kernel, o.stream);
+    }
+};
+
+struct Entry {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int* chunk_row = nullptr;
+    void* bt = nullptr;       // B in the other layout (may be null: see twin fallback)
+    int* own_kernel = nullptr;
+    ~Entry() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        cudaFree(chunk_row);
+        cudaFree(bt);
+        cudaFree(own_kernel);
+    }
+};
+
+struct Cache {
+    std::mutex mu;
+    std::map<Key, std::unique_ptr<Entry>> entries;
+};
+
+int elem(int dtype) { return dtype == DASPMM_F64 ? 8 : 4; }
+
+}  // namespace
+
+void graph_cache_free(daspmm_csr* h) {
+    delete static_cast<Cache*>(h->graph_cache);
+    h->graph_cache = nullptr;
+}
+
+static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k, Entry& en) {
+    cudaError_t e;
+    int* d_kernel = k.d_kernel;
+    if (!d_kernel) {
+        if ((e = cudaMalloc(&en.own_kernel, sizeof(int))) != cudaSuccess)
+            return cuda_fail(e, "graph: cudaMalloc");
+        d_kernel = en.own_kernel;
+    }
+    // Scratch: EB chunk rows for the largest plan, and B in the other layout.
+    int64_t max_p = 1;
+    for (int kid = 4; kid < 8; ++kid) {
+        const Plan p = plan_spmm(h, kid, 0, k.W, k.N, k.B, k.ldb, k.C, k.ldc,
+                                 (k.flags & DASPMM_EXACT) != 0);
+        max_p = std::max<int64_t>(max_p, p.P);
+    }
+    if ((e = cudaMalloc(&en.chunk_row, sizeof(int) * size_t(max_p))) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaMalloc(chunk_row)");
+    const size_t bt_bytes = size_t(elem(h->dtype)) * size_t(h->K) * size_t(k.N);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (bt_bytes > 0 && bt_bytes <= free_b / 4) {
+        if ((e = cudaMalloc(&en.bt, bt_bytes)) != cudaSuccess) en.bt = nullptr;
+    }
+    const int64_t ldt = k.b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
+                                                       : std::max<int64_t>(k.N, 1);
+
+    cudaStream_t cap;
+    if ((e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "graph: stream");
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{cap};
+
+    if ((e = cudaGraphCreate(&en.graph, 0)) != cudaSuccess) return cuda_fail(e, "graph: create");
+    cudaGraphConditionalHandle cond;
+    if ((e = cudaGraphConditionalHandleCreate(&cond, en.graph, 8u, cudaGraphCondAssignDefault)) !=
+        cudaSuccess)
+        return cuda_fail(e, "graph: conditional handle");
+    // Node 0: selector.
+    if ((e = cudaStreamBeginCaptureToGraph(cap, en.graph, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return cuda_fail(e, "graph: capture(select)");
+    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap);
+    cudaGraph_t g_out = nullptr;
+    e = cudaStreamEndCapture(cap, &g_out);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "graph: end capture(select)");
+    size_t n_nodes = 0;
+    cudaGraphGetNodes(en.graph, nullptr, &n_nodes);
+    std::vector<cudaGraphNode_t> nodes(n_nodes);
+    cudaGraphGetNodes(en.graph, nodes.data(), &n_nodes);
+    // Node 1: SWITCH over the eight design-space kernels.
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeSwitch;
+    cp.conditional.size = 8;
+    cudaGraphNode_t sw;
+    if ((e = cudaGraphAddNode(&sw, en.graph, nodes.data(), n_nodes, &cp)) != cudaSuccess)
+        return cuda_fail(e, "graph: add switch node");
+    for (int kid = 0; kid < 8; ++kid) {
+        cudaGraph_t body = cp.conditional.phGraph_out[kid];
+        const int want = ((kid >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
+        int run_kid = kid;
+        const void* Bk = k.B;
+        int64_t ldk = k.ldb;
+        bool need_t = want != k.b_layout;
+        if (need_t && !en.bt) {
+            run_kid = kid ^ 2;  // layout twin: same M/K choices, operand's layout
+            need_t = false;
+        }
+        if ((e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+            return cuda_fail(e, "graph: capture(body)");
+        if (need_t) {
+            if (k.b_layout == DASPMM_ROW_MAJOR)
+                e = transpose(h->dtype, k.B, h->K, k.N, k.ldb, en.bt, ldt, cap);
+            else
+                e = transpose(h->dtype, k.B, k.N, h->K, k.ldb, en.bt, ldt, cap);
+            Bk = en.bt;
+            ldk = ldt;
+        }
+        // make_config defaults (worker.hpp:47-55): W = 8 unless given.
+        rc = e == cudaSuccess ? spmm_device(h, run_kid, 0, k.W, Bk, ldk, k.N, k.C, k.ldc, k.flags,
+                                            cap, en.chunk_row)
+                              : cuda_fail(e, "graph: transpose");
+        cudaGraph_t bo = nullptr;
+        e = cudaStreamEndCapture(cap, &bo);
+        if (rc) return rc;
+        if (e != cudaSuccess) return cuda_fail(e, "graph: end capture(body)");
+    }
+    if ((e = cudaGraphInstantiate(&en.exec, en.graph, 0)) != cudaSuccess)
+        return cuda_fail(e, "graph: instantiate");
+    return DASPMM_OK;
+}
+
+}  // namespace daspmm
+
+using namespace daspmm;
+
+extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, int64_t hw,
+                                    const void* d_B, int b_layout, int64_t ldb, int64_t N,
+                                    void* d_C, int64_t ldc, int64_t W, unsigned flags,
+                                    int* d_kernel, daspmm_stream stream) {
+    if (!h || !m) return fail(DASPMM_ERR_INVALID_ARG, "spmm_selected: null argument");
+    if (W <= 0) W = 8;
+    const int want_kernel0 = b_layout == DASPMM_COL_MAJOR ? 2 : 0;
+    if (int rc = check_call(h, want_kernel0, 0, W, 1, b_layout, ldb, N, ldc,
+                            (flags & DASPMM_EXACT) != 0))
+        return rc;
+    if (h->M == 0)
+        return fail(DASPMM_ERR_INVALID_ARG, "extract_features: matrix has no rows to summarize");
+    int nc = 0, nf = 0, nr = 0, uh = 0;
+    daspmm_model_info(m, &nc, &nf, &nr, &uh);
+    if (uh && hw < 0)
+        return fail(DASPMM_ERR_INVALID_ARG,
+                    "encode_features: model expects a hardware_id but the sample has none");
+    if (nf != (uh ? 5 : 4)) return fail(DASPMM_ERR_INVALID_ARG, "predict: feature count mismatch");
+    if (N == 0) return DASPMM_OK;
+    DeviceGuard g(h->device);
+    daspmm_csr* hm = const_cast<daspmm_csr*>(h);
+    {
+        std::lock_guard<std::mutex> lk(hm->mu);
+        if (!hm->graph_cache) hm->graph_cache = new Cache;
+    }
+    Cache* cache = static_cast<Cache*>(hm->graph_cache);
+    const Key key{model_generation(m), d_B, b_layout, ldb, N, d_C, ldc, W, flags, uh ? hw : -1,
+                  d_kernel, static_cast<cudaStream_t>(stream)};
+    Entry* en = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(cache->mu);
+        auto it = cache->entries.find(key);
+        if (it == cache->entries.end()) {
+            auto fresh = std::make_unique<Entry>();
+            if (int rc = build_entry(h, m, key, *fresh)) return rc;
+            it = cache->entries.emplace(key, std::move(fresh)).first;
+        }
+        en = it->second.get();
+    }
+    cudaError_t e = cudaGraphLaunch(en->exec, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "graph launch");
+}

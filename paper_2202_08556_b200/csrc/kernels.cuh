@@ -1,0 +1,447 @@
+// daspmm — the eight DA-SpMM kernels (2 x 2 x 2 design space, §3) as
+// hand-written sm_100a CUDA. Each kernel restates one reference worker body
+// (proj/include/spmmkit/spmm.hpp:40-187) for the GPU execution model:
+//
+//   M-loop  RB : a lane group owns a row (spmm.hpp:66-107)
+//           EB : a lane group owns an equal-nnz chunk, partition.hpp:45-64 bounds
+//                (spmm.hpp:108-186); split rows take atomics, owned rows plain stores
+//   N-loop  RM : B row-major, V-wide vector gathers (Technique 2)
+//           CM : B column-major, scalar gathers at stride ldb
+//   K-loop  SR : lanes span columns, each lane accumulates its columns sequentially
+//                in nnz order (spmm.hpp:85-88, 145-159)
+//           PR : lanes span nonzeros; W-lane adjacent-pair tree (RB, reduce.hpp:18-25)
+//                or gated conditional scan (EB, Technique 4, reduce.hpp:31-39)
+//
+// Coalesced row caching (CRC / Technique 3): A's (col, val) pairs are loaded once per
+// step with coalesced per-lane loads and broadcast through register shuffles, so
+// every B gather of a step reuses them across all columns the group owns.
+//
+// Launch shape: 256-thread CTAs; groups of LPR (SR) or W (PR) lanes; blockIdx.y
+// walks column tiles. Element offsets are int32 (nnz < 2^31).
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace daspmm {
+
+template <typename T>
+struct SpmmArgs {
+    const int* __restrict__ rp;  // M+1 row offsets
+    const int* __restrict__ ci;  // nnz column indices
+    const T* __restrict__ va;    // nnz values
+    const T* __restrict__ B;     // K x N, RM (ldb >= N) or CM (ldb >= K)
+    T* C;                        // M x N row-major, ldc >= N
+    int M, K, N;
+    int64_t nnz, ldb, ldc;
+    int64_t P;                   // EB workers (chunks)
+    int seg;                     // exact-mode EB+SR staging segment, max(W, 256)
+    int64_t rpg;                 // RB: rows per group (row-block size)
+    const int* __restrict__ chunk_row;  // EB: row holding each chunk's first element
+};
+
+constexpr int kThreads = 256;
+
+template <typename T, bool CM, int V>
+__device__ __forceinline__ Frag<T, V> gather(const SpmmArgs<T>& a, int k, int col) {
+    if constexpr (CM) return ld_frag_cm<T, V>(a.B + int64_t(col) * a.ldb + k, a.ldb);
+    else return ld_frag<T, V>(a.B + int64_t(k) * a.ldb + col);
+}
+
+// =============================================================== SR walker (K0/K2/K4/K6)
+// One lane group of LPR lanes walks a contiguous nonzero range [e0, e1) in order,
+// lane gl owning columns n0 + s*LPR*V + [0, V), s < CPL. Per step it holds STEP
+// (col, val) pairs in registers (coalesced loads, Technique 3 / CRC) and broadcasts
+// them by shuffle; the NEXT step's pairs are loaded before this step's B gathers are
+// issued, so A's load latency overlaps the gathers instead of preceding them.
+// Accumulation per column is sequential in nnz order (spmm.hpp:85-88, 145-159).
+//
+//   RB (K0/K2): the range is exactly the rows [r, r_end) of a row block — every row
+//               is owned, stored once; empty rows receive zeros.
+//   EB (K4/K6): the range is partition chunk w; rows cut by the range ends are split
+//               and take atomics (pre-zeroed by k_eb_prep); empty rows pre-zeroed.
+//               Exact mode restarts the run at the reference's staging boundaries
+//               (seg_cap = max(W, 256), spmm.hpp:50, 136) and adds the partials in
+//               the reference's order.
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, bool EB>
+__device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, const int e1, int r,
+                                        const int r_end, const int n0, const unsigned mask,
+                                        const int gl) {
+    constexpr int STEP = LPR >= 16 ? LPR : (LPR >= 4 ? 16 : 8);  // pairs per group per step
+    constexpr int EPL = STEP / LPR;                              // pairs per lane per step
+    // Double-buffered A pairs pay off once a lane holds few of them (LPR >= 4); narrow
+    // groups rely on occupancy instead and keep the registers for gathers.
+    constexpr bool PREFETCH = LPR >= 4;
+    constexpr int WORDS = V * CPL * int(sizeof(T)) / 4;  // accumulator registers per lane
+    constexpr int BATCH0 = WORDS >= 8 ? 2 : (WORDS >= 4 ? 4 : 8);
+    constexpr int BATCH = BATCH0 < STEP ? BATCH0 : STEP;  // gathers in flight per lane
+    Frag<T, V> acc[CPL], ydep[CPL];
+#pragma unroll
+    for (int s = 0; s < CPL; ++s)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[s].v[i] = ydep[s].v[i] = T(0);
+    int rstart = __ldg(a.rp + r), rend = __ldg(a.rp + r + 1);
+    bool has = false;
+    int next_seg = e0 + a.seg;
+
+    auto flush = [&]() {  // row r is complete within this range
+        if (EB && !has) return;
+        const bool owned = !EB || (rstart >= e0 && rend <= e1);
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+            Frag<T, V> out;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                out.v[i] = (EB && EXACT) ? add_rn(ydep[s].v[i], acc[s].v[i]) : acc[s].v[i];
+                acc[s].v[i] = ydep[s].v[i] = T(0);
+            }
+            const int col = n0 + s * LPR * V;
+            if (col < a.N) {
+                T* y = a.C + int64_t(r) * a.ldc + col;
+                if (owned) st_frag(y, out);
+                else atomic_add_frag(y, out);
+            }
+        }
+        has = false;
+    };
+
+    int c[EPL];
+    T v[EPL];
+    if constexpr (PREFETCH) {
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) {
+            const int e = e0 + q * LPR + gl;
+            c[q] = e < e1 ? ld_stream(a.ci + e) : 0;
+            v[q] = e < e1 ? ld_stream(a.va + e) : T(0);
+        }
+    }
+    for (int j = e0; j < e1; j += STEP) {
+        int cn[PREFETCH ? EPL : 1];
+        T vn[PREFETCH ? EPL : 1];
+        if constexpr (PREFETCH) {
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {  // prefetch the next step
+                const int e = j + STEP + q * LPR + gl;
+                cn[q] = e < e1 ? ld_stream(a.ci + e) : 0;
+                vn[q] = e < e1 ? ld_stream(a.va + e) : T(0);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {
+                const int e = j + q * LPR + gl;
+                c[q] = e < e1 ? ld_stream(a.ci + e) : 0;
+                v[q] = e < e1 ? ld_stream(a.va + e) : T(0);
+            }
+        }
+        const int cnt = min(STEP, e1 - j);
+#pragma unroll
+        for (int x0 = 0; x0 < STEP; x0 += BATCH) {
+            if (x0 < cnt) {  // group-uniform
+                const int nb = min(BATCH, cnt - x0);
+                T vv[BATCH];
+                Frag<T, V> b[BATCH][CPL];
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const int x = x0 + u;
+                    const int ct = gshfl<LPR>(mask, c[x / LPR], x % LPR);
+                    vv[u] = gshfl<LPR>(mask, v[x / LPR], x % LPR);
+                    // padded tail entries gather row 0 of B harmlessly and are never summed
+#pragma unroll
+                    for (int s = 0; s < CPL; ++s) {
+                        const int col = n0 + s * LPR * V;
+                        if (col < a.N) b[u][s] = gather<T, CM, V>(a, u < nb ? ct : 0, col);
+                    }
+                }
+                const int ef = j + x0;
+                const bool seg_in_batch = EB && EXACT && next_seg >= ef && next_seg < ef + nb;
+                if (nb == BATCH && ef + BATCH <= rend && !seg_in_batch) {
+                    // fast path: the whole batch continues the current row
+#pragma unroll
+                    for (int u = 0; u < BATCH; ++u)
+#pragma unroll
+                        for (int s = 0; s < CPL; ++s)
+#pragma unroll
+                            for (int i = 0; i < V; ++i)
+                                acc[s].v[i] = madd<EXACT>(acc[s].v[i], vv[u], b[u][s].v[i]);
+                    has = true;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < BATCH; ++u) {
+                        if (u < nb) {
+                            const int e = ef + u;
+                            while (e >= rend) {  // row change; steps over empty rows
+                                flush();
+                                ++r;
+                                rstart = rend;
+                                rend = __ldg(a.rp + r + 1);
+                            }
+                            if constexpr (EB && EXACT) {
+                                if (e == next_seg) {  // reference staging boundary
+#pragma unroll
+                                    for (int s = 0; s < CPL; ++s)
+#pragma unroll
+                                        for (int i = 0; i < V; ++i) {
+                                            ydep[s].v[i] = add_rn(ydep[s].v[i], acc[s].v[i]);
+                                            acc[s].v[i] = T(0);
+                                        }
+                                    next_seg += a.seg;
+                                }
+                            }
+                            has = true;
+#pragma unroll
+                            for (int s = 0; s < CPL; ++s)
+#pragma unroll
+                                for (int i = 0; i < V; ++i)
+                                    acc[s].v[i] = madd<EXACT>(acc[s].v[i], vv[u], b[u][s].v[i]);
+                        }
+                    }
+                }
+            }
+        }
+        if constexpr (PREFETCH) {
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {
+                c[q] = cn[q];
+                v[q] = vn[q];
+            }
+        }
+    }
+    flush();
+    if constexpr (!EB) {  // trailing empty rows of the block
+        for (++r; r < r_end; ++r) flush();
+    }
+}
+
+// RB + SR: group g owns rows [g*rpg, (g+1)*rpg) — a row block, balanced by row count.
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4) k_rb_sr(const SpmmArgs<T> a) {
+    constexpr int TN = LPR * V * CPL;
+    const unsigned mask = group_mask<LPR>();
+    const int gl = threadIdx.x & (LPR - 1);
+    const int64_t g = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    const int64_t r0 = g * a.rpg;
+    if (r0 >= a.M) return;  // whole group leaves together
+    const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
+    const int n0 = blockIdx.y * TN + gl * V;
+    sr_walk<T, CM, EXACT, V, LPR, CPL, false>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0), r1,
+                                              n0, mask, gl);
+}
+
+// EB + SR: group w owns partition chunk w (partition.hpp:45-64).
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4) k_eb_sr(const SpmmArgs<T> a) {
+    constexpr int TN = LPR * V * CPL;
+    const unsigned mask = group_mask<LPR>();
+    const int gl = threadIdx.x & (LPR - 1);
+    const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    if (w >= a.P) return;
+    int64_t e0, e1;
+    chunk_bounds(a.nnz, a.P, w, e0, e1);
+    if (e0 >= e1) return;
+    const int n0 = blockIdx.y * TN + gl * V;
+    sr_walk<T, CM, EXACT, V, LPR, CPL, true>(a, int(e0), int(e1), a.chunk_row[w], a.M, n0, mask,
+                                             gl);
+}
+
+// =============================================================== RB + PR (K1 / K3)
+// W lanes per row step through the row in W-wide tiles (Technique 1 for-loop);
+// each column slot's tile products go through the adjacent-pair tree, and the
+// slot's owner lane (slot % W) carries the row accumulator: y += tile_sum per
+// tile, the reference's RB+PR order (spmm.hpp:93-103).
+template <typename T, bool CM, bool EXACT, int V, int W, int OWN>
+__global__ void __launch_bounds__(kThreads) k_rb_pr(const SpmmArgs<T> a) {
+    constexpr int NSLOT = W * OWN;  // column slots per tile (V columns each)
+    constexpr int U = NSLOT < 4 ? NSLOT : 4;
+    const unsigned mask = group_mask<W>();
+    const int gl = threadIdx.x & (W - 1);
+    const int64_t row = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / W;
+    if (row >= a.M) return;
+    const int nbase = blockIdx.y * NSLOT * V;
+
+    Frag<T, V> acc[OWN];
+#pragma unroll
+    for (int o = 0; o < OWN; ++o)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[o].v[i] = T(0);
+
+    const int rs = __ldg(a.rp + row), re = __ldg(a.rp + row + 1);
+    for (int j = rs; j < re; j += W) {
+        const int e = j + gl;
+        const bool valid = e < re;
+        const int c = valid ? ld_stream(a.ci + e) : 0;
+        const T v = valid ? ld_stream(a.va + e) : T(0);
+#pragma unroll
+        for (int s0 = 0; s0 < NSLOT; s0 += U) {
+            Frag<T, V> b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int col = nbase + (s0 + u) * V;
+                if (valid && col < a.N) b[u] = gather<T, CM, V>(a, c, col);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int s = s0 + u;
+                const int col = nbase + s * V;
+                if (col < a.N) {  // group-uniform
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        // padded lanes contribute +0 exactly as the reference pads (spmm.hpp:98-99)
+                        T p = valid ? (EXACT ? mul_rn(v, b[u].v[i]) : v * b[u].v[i]) : T(0);
+                        p = group_tree_sum<W>(mask, p);
+                        if ((s % W) == gl)
+                            acc[s / W].v[i] = EXACT ? add_rn(acc[s / W].v[i], p) : acc[s / W].v[i] + p;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < OWN; ++o) {
+        const int s = o * W + gl;
+        const int col = nbase + s * V;
+        if (col < a.N) st_frag(a.C + row * a.ldc + col, acc[o]);
+    }
+}
+
+// =============================================================== EB prep
+// partition_elements on the device (partition.hpp:45-64) for P chunks: the row of
+// each chunk's first element by binary search (upper_bound - 1), M for empty tail
+// chunks. A chunk whose first row began in an earlier chunk marks that row as
+// split: it is zeroed here so the EB kernels can deposit into it with atomics.
+// Empty rows (never touched by an EB walker) are zeroed from the handle's list.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+k_eb_prep(const int* __restrict__ rp, int M, int64_t nnz, int64_t P, int* __restrict__ chunk_row,
+          T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty) {
+    const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (tid < P) {
+        int64_t b, e;
+        chunk_bounds(nnz, P, tid, b, e);
+        const int row = b < nnz ? row_of_element(rp, M, int(b)) : M;
+        chunk_row[tid] = row;
+        if (b < nnz && __ldg(rp + row) < b) {
+            T* y = C + int64_t(row) * ldc;
+            for (int n = 0; n < N; ++n) y[n] = T(0);
+        }
+    } else if (tid - P < int64_t(n_empty) * N) {
+        const int64_t k = tid - P;
+        const int r = empty_rows[k / N];
+        C[int64_t(r) * ldc + k % N] = T(0);
+    }
+}
+
+// =============================================================== EB + PR (K5 / K7)
+// W lanes take W consecutive nonzeros of the chunk (tiles at e0 + m*W, as the
+// reference's groups, spmm.hpp:164-183). Each lane resolves its element's row with
+// a shuffle binary search over W row offsets, the gated scan sums each row run,
+// and the run's first lane deposits: a row owned by the chunk is stored on its
+// first tile and read-modify-written on later tiles (y += seg, the reference's
+// deposit order), a split row takes an atomic add.
+template <int W>
+__device__ __forceinline__ void resolve_rows(unsigned mask, const int* __restrict__ rp, int M,
+                                             int e, bool valid, int cur, int cur_start,
+                                             int& row, int& rs, int& re) {
+    int base = cur, base_start = cur_start;
+    bool done = !valid;
+    row = M;
+    rs = re = 0;
+    while (true) {
+        const int idx = base + 1 + (threadIdx.x & (W - 1));
+        const int b = idx <= M ? __ldg(rp + idx) : INT_MAX;
+        const int blast = __shfl_sync(mask, b, W - 1, W);
+        int cnt = 0;
+#pragma unroll
+        for (int s = W / 2; s >= 1; s >>= 1) {
+            const int bb = __shfl_sync(mask, b, cnt + s - 1, W);
+            if (bb <= e) cnt += s;
+        }
+        const int bprev = __shfl_sync(mask, b, cnt > 0 ? cnt - 1 : 0, W);
+        const int bcur = __shfl_sync(mask, b, cnt, W);
+        if (!done && e < blast) {
+            row = base + cnt;
+            rs = cnt > 0 ? bprev : base_start;
+            re = bcur;
+            done = true;
+        }
+        if (!__any_sync(mask, !done)) break;
+        base += W;
+        base_start = blast;
+    }
+}
+
+template <typename T, bool CM, bool EXACT, int V, int W, int OWN>
+__global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
+    constexpr int NSLOT = W * OWN;
+    constexpr int U = NSLOT < 4 ? NSLOT : 4;
+    const unsigned mask = group_mask<W>();
+    const int gl = threadIdx.x & (W - 1);
+    const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / W;
+    if (w >= a.P) return;
+    int64_t e0l, e1l;
+    chunk_bounds(a.nnz, a.P, w, e0l, e1l);
+    if (e0l >= e1l) return;
+    const int e0 = int(e0l), e1 = int(e1l);
+    const int nbase = blockIdx.y * NSLOT * V;
+
+    int cur = a.chunk_row[w];
+    int cur_start = __ldg(a.rp + cur);
+    for (int tb = e0; tb < e1; tb += W) {
+        const int e = tb + gl;
+        const bool valid = e < e1;
+        const int c = valid ? ld_stream(a.ci + e) : 0;
+        const T v = valid ? ld_stream(a.va + e) : T(0);
+        int row, rs, re;
+        resolve_rows<W>(mask, a.rp, a.M, e, valid, cur, cur_start, row, rs, re);
+        const int id = valid ? row : a.M;  // sentinel pads the tile (spmm.hpp:167)
+        const unsigned gates = scan_gates<W>(mask, id, gl);
+        const int prev_id = __shfl_up_sync(mask, id, 1, W);
+        const bool seg_start = valid && (gl == 0 || prev_id != id);
+        const bool owned = rs >= e0 && re <= e1;
+        const bool first = (e == rs);
+#pragma unroll
+        for (int s0 = 0; s0 < NSLOT; s0 += U) {
+            Frag<T, V> b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int col = nbase + (s0 + u) * V;
+                if (valid && col < a.N) b[u] = gather<T, CM, V>(a, c, col);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int col = nbase + (s0 + u) * V;
+                if (col < a.N) {  // group-uniform
+                    Frag<T, V> p;
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        p.v[i] = valid ? (EXACT ? mul_rn(v, b[u].v[i]) : v * b[u].v[i]) : T(0);
+                        p.v[i] = group_conditional_scan_gated<W>(mask, p.v[i], gates);
+                    }
+                    if (seg_start) {
+                        T* y = a.C + int64_t(row) * a.ldc + col;
+                        if (!owned) {
+                            atomic_add_frag(y, p);
+                        } else if (first) {
+                            if constexpr (EXACT) {
+#pragma unroll
+                                for (int i = 0; i < V; ++i) p.v[i] = add_rn(T(0), p.v[i]);
+                            }
+                            st_frag_rw(y, p);
+                        } else {
+                            Frag<T, V> old = ld_frag_rw<T, V>(y);
+#pragma unroll
+                            for (int i = 0; i < V; ++i) p.v[i] = add_rn(old.v[i], p.v[i]);
+                            st_frag_rw(y, p);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp(mask);  // orders this tile's owned-row stores before the next tile's RMW
+        const int last = min(W, e1 - tb) - 1;
+        cur = __shfl_sync(mask, row, last, W);
+        cur_start = __shfl_sync(mask, rs, last, W);
+    }
+}
+
+}  // namespace daspmm

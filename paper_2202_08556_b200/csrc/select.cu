@@ -1,0 +1,422 @@
+// daspmm — the data-aware selector (paper §5; selector.hpp, gbdt.hpp).
+//
+// Host side: parse the reference's selector text v1 (selector.hpp:113-132,
+// gbdt.hpp:336-453) with the same validation and messages, keep the ensemble, and
+// evaluate predict_kernel exactly as the reference (selector.hpp:62-65).
+//
+// Device side: the ensemble is flattened once. Every split is rewritten into an
+// exact integer or interval test so the GPU decision cannot drift from the host's:
+//   f0 = log2(max(nnz,1))  <= t   <=>  max(nnz,1)  <= icut  (icut found with the host's
+//   f1 = log2(max(M,1))    <= t   <=>  max(M,1)    <= icut   own std::log2, so CUDA's
+//                                                            log2 never enters)
+//   f3 = (double)N         <= t   <=>  N   <= floor(t)
+//   f4 = (double)hw        <= t   <=>  hw  <= floor(t)
+//   f2 = std_row           <= t   decided from the handle's proven interval
+//                                  [std_lo, std_hi]; if t falls inside it the kernel
+//                                  replays the reference's sequential sum (cached).
+// Per-class raw scores are then summed in round order with __dadd_rn and the argmax
+// uses strict '>' (ties to the lowest class), as gbdt.hpp:60-77.
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace daspmm {
+
+struct HostNode {
+    int feature = -1;
+    double threshold = 0.0;
+    int left = -1, right = -1;
+    double value = 0.0;
+};
+
+struct DevNode {
+    int feature;  // -1 leaf
+    int left;     // absolute node index
+    int right;
+    int pad;
+    double thr;   // std_row threshold (feature 2)
+    long long icut;  // integer cut for features 0, 1, 3, 4
+    double value;
+};
+
+}  // namespace daspmm
+
+struct daspmm_model {
+    uint64_t generation = 0;  // unique per parse; keys graph caches
+    int num_classes = 0, num_features = 0, best_round = -1;
+    bool uses_hardware = false;
+    std::vector<std::vector<std::vector<daspmm::HostNode>>> rounds;  // [round][class]
+    std::vector<int64_t> tree_off;                                  // flattened
+    daspmm::DevNode* d_nodes = nullptr;
+    int64_t* d_tree_off = nullptr;
+    int64_t n_nodes = 0;
+};
+
+namespace daspmm {
+
+namespace {
+
+struct Parser {
+    std::istringstream in;
+    explicit Parser(std::string s) : in(std::move(s)) {}
+    std::string err;
+    template <class T>
+    bool tok(T& v, const char* what) {
+        if (!(in >> v)) {
+            err = std::string("model stream truncated or malformed: expected ") + what;
+            return false;
+        }
+        return true;
+    }
+    bool lit(const std::string& l) {
+        std::string t;
+        if (!tok(t, l.c_str())) return false;
+        if (t != l) {
+            err = "model stream malformed: expected '" + l + "', got '" + t + "'";
+            return false;
+        }
+        return true;
+    }
+};
+
+// Largest n >= 1 with std::log2((double)n) <= t, or 0 when none (t < 0).
+long long log2_cut(double t) {
+    if (!(std::log2(1.0) <= t)) return 0;
+    long long lo = 1, hi = (1LL << 62);
+    if (std::log2(double(hi)) <= t) return hi;
+    while (hi - lo > 1) {
+        const long long mid = lo + (hi - lo) / 2;
+        if (std::log2(double(mid)) <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+long long floor_cut(double t) {
+    if (t >= 9.0e18) return (1LL << 62);
+    if (t < -9.0e18) return -(1LL << 62);
+    return (long long)std::floor(t);
+}
+
+}  // namespace
+
+int parse_model(const char* text, size_t len, daspmm_model** out) {
+    Parser p(std::string(text, len));
+    auto bad = [&](const std::string& m) { return fail(DASPMM_ERR_MODEL_FORMAT, m); };
+    std::string tag, ver;
+    if (!p.tok(tag, "selector tag") || !p.tok(ver, "selector version")) return bad(p.err);
+    if (tag != "spmmkit-selector") return bad("not a selector stream (tag '" + tag + "')");
+    if (ver != "v1") return bad("unsupported selector version '" + ver + "', expected v1");
+    int uses_hw = 0;
+    if (!p.lit("uses_hardware") || !p.tok(uses_hw, "uses_hardware flag")) return bad(p.err);
+    if (!p.tok(tag, "format tag") || !p.tok(ver, "format version")) return bad(p.err);
+    if (tag != "spmmkit-gbdt") return bad("not a model stream (tag '" + tag + "')");
+    if (ver != "v1") return bad("unsupported model version '" + ver + "', expected v1");
+    auto* m = new daspmm_model;
+    static std::atomic<uint64_t> gen{1};
+    m->generation = gen++;
+    std::unique_ptr<daspmm_model> guard(m);
+    m->uses_hardware = uses_hw != 0;
+    if (!p.lit("classes") || !p.tok(m->num_classes, "class count") || !p.lit("features") ||
+        !p.tok(m->num_features, "feature count") || !p.lit("best_round") ||
+        !p.tok(m->best_round, "best round"))
+        return bad(p.err);
+    if (m->num_classes < 1 || m->num_features < 0) return bad("implausible class/feature counts");
+    if (!p.lit("config")) return bad(p.err);
+    {  // GbdtConfig fields with their reference types (gbdt.hpp:396-409)
+        int iv;
+        double dv;
+        unsigned long long uv;
+        if (!p.lit("num_rounds") || !p.tok(iv, "num_rounds") || !p.lit("max_depth") ||
+            !p.tok(iv, "max_depth") || !p.lit("min_leaf") || !p.tok(iv, "min_leaf") ||
+            !p.lit("learning_rate") || !p.tok(dv, "learning_rate") || !p.lit("patience") ||
+            !p.tok(iv, "patience") || !p.lit("lambda") || !p.tok(dv, "lambda") ||
+            !p.lit("seed") || !p.tok(uv, "seed"))
+            return bad(p.err);
+    }
+    int n_names = 0;
+    if (!p.lit("feature_names") || !p.tok(n_names, "feature name count")) return bad(p.err);
+    if (n_names < 0 || n_names > 4096) return bad("implausible feature name count");
+    for (int i = 0; i < n_names; ++i) {
+        std::string nm;
+        if (!p.tok(nm, "feature name")) return bad(p.err);
+    }
+    int n_rounds = 0;
+    if (!p.lit("rounds") || !p.tok(n_rounds, "round count")) return bad(p.err);
+    if (n_rounds < 0 || n_rounds > 1000000) return bad("implausible round count");
+    m->rounds.resize(n_rounds);
+    for (int r = 0; r < n_rounds; ++r) {
+        m->rounds[r].resize(m->num_classes);
+        for (int c = 0; c < m->num_classes; ++c) {
+            int rr = 0, cc = 0, nn = 0;
+            if (!p.lit("tree") || !p.tok(rr, "tree round") || !p.tok(cc, "tree class"))
+                return bad(p.err);
+            if (rr != r || cc != c) return bad("tree out of order");
+            if (!p.tok(nn, "node count")) return bad(p.err);
+            if (nn < 1 || nn > 10000000) return bad("implausible node count");
+            auto& tree = m->rounds[r][c];
+            tree.resize(nn);
+            for (auto& nd : tree) {
+                std::string kind;
+                if (!p.lit("node") || !p.tok(kind, "node kind")) return bad(p.err);
+                if (kind == "split") {
+                    double gain;
+                    if (!p.tok(nd.feature, "split feature") || !p.tok(nd.threshold, "split threshold") ||
+                        !p.tok(nd.left, "left child") || !p.tok(nd.right, "right child") ||
+                        !p.tok(gain, "split gain"))
+                        return bad(p.err);
+                    if (nd.feature >= m->num_features || nd.left < 0 || nd.right < 0 ||
+                        nd.left >= nn || nd.right >= nn)
+                        return bad("split node references out of range");
+                } else if (kind == "leaf") {
+                    nd.feature = -1;
+                    if (!p.tok(nd.value, "leaf value")) return bad(p.err);
+                } else {
+                    return bad("unknown node kind '" + kind + "'");
+                }
+            }
+        }
+    }
+    if (!p.lit("end")) return bad(p.err);
+
+    // Flatten and upload.
+    std::vector<DevNode> nodes;
+    m->tree_off.push_back(0);
+    for (int r = 0; r < n_rounds; ++r)
+        for (int c = 0; c < m->num_classes; ++c) {
+            const auto& tree = m->rounds[r][c];
+            const int base = int(nodes.size());
+            for (const auto& nd : tree) {
+                DevNode d{};
+                d.feature = nd.feature;
+                d.left = nd.left >= 0 ? base + nd.left : -1;
+                d.right = nd.right >= 0 ? base + nd.right : -1;
+                d.thr = nd.threshold;
+                d.value = nd.value;
+                if (nd.feature == 0 || nd.feature == 1) d.icut = log2_cut(nd.threshold);
+                else if (nd.feature >= 3) d.icut = floor_cut(nd.threshold);
+                nodes.push_back(d);
+            }
+            m->tree_off.push_back(int64_t(nodes.size()));
+        }
+    m->n_nodes = int64_t(nodes.size());
+    if (daspmm_device_count() > 0 && !nodes.empty()) {
+        cudaError_t e;
+        if ((e = cudaMalloc(&m->d_nodes, sizeof(DevNode) * nodes.size())) != cudaSuccess ||
+            (e = cudaMalloc(&m->d_tree_off, sizeof(int64_t) * m->tree_off.size())) != cudaSuccess)
+            return cuda_fail(e, "model upload");
+        cudaMemcpy(m->d_nodes, nodes.data(), sizeof(DevNode) * nodes.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(m->d_tree_off, m->tree_off.data(), sizeof(int64_t) * m->tree_off.size(),
+                   cudaMemcpyHostToDevice);
+    }
+    *out = guard.release();
+    return DASPMM_OK;
+}
+
+// encode_features (selector.hpp:19-33) + predict_class (gbdt.hpp:60-77) on the host.
+int predict_host(const daspmm_model* m, int64_t nnz, int64_t mat_size, double std_row,
+                 int64_t n_cols, int64_t hw, int* kernel) {
+    std::vector<double> f{std::log2(double(std::max<int64_t>(nnz, 1))),
+                          std::log2(double(std::max<int64_t>(mat_size, 1))), std_row,
+                          double(n_cols)};
+    if (m->uses_hardware) {
+        if (hw < 0)
+            return fail(DASPMM_ERR_INVALID_ARG,
+                        "encode_features: model expects a hardware_id but the sample has none");
+        f.push_back(double(hw));
+    }
+    if (int(f.size()) != m->num_features)
+        return fail(DASPMM_ERR_INVALID_ARG, "predict: got " + std::to_string(f.size()) +
+                                                " features, model expects " +
+                                                std::to_string(m->num_features));
+    std::vector<double> s(m->num_classes, 0.0);
+    for (const auto& round : m->rounds)
+        for (int c = 0; c < m->num_classes; ++c) {
+            const auto& t = round[c];
+            int i = 0;
+            while (t[i].feature >= 0) i = f[t[i].feature] <= t[i].threshold ? t[i].left : t[i].right;
+            s[c] += t[i].value;
+        }
+    int best = 0;
+    for (int c = 1; c < m->num_classes; ++c)
+        if (s[c] > s[best]) best = c;
+    if (best < 0 || best > 7) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
+    *kernel = best;
+    return DASPMM_OK;
+}
+
+// ------------------------------------------------------------------ device selector
+constexpr int kSelThreads = 256;
+constexpr int kMaxClasses = 16;
+
+// Decision for one split; returns 0/1, or 2 when the std interval is ambiguous.
+__device__ __forceinline__ int decide(const DevNode& nd, long long f0, long long f1, long long f3,
+                                      long long f4, double std_lo, double std_hi, bool have_exact,
+                                      double std_exact) {
+    switch (nd.feature) {
+        case 0: return f0 <= nd.icut;
+        case 1: return f1 <= nd.icut;
+        case 3: return f3 <= nd.icut;
+        case 4: return f4 <= nd.icut;
+        default:
+            if (have_exact) return std_exact <= nd.thr;
+            if (nd.thr < std_lo) return 0;
+            if (nd.thr >= std_hi) return 1;
+            return 2;
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off, int num_rounds,
+         int num_classes, const int* __restrict__ rp, DevFeatures* feat, long long n_cols,
+         long long hw, int* out_kernel, cudaGraphConditionalHandle cond, int use_cond) {
+    extern __shared__ double leaf[];  // [num_rounds * num_classes]
+    __shared__ int ambiguous;
+    __shared__ double s_exact;
+    __shared__ int s_have;
+    __shared__ double scores[kMaxClasses];
+    if (threadIdx.x == 0) {
+        ambiguous = 0;
+        s_have = feat->exact_valid;
+        s_exact = feat->std_exact;
+    }
+    __syncthreads();
+    const long long nnz = feat->nnz > 1 ? feat->nnz : 1;
+    const long long rows = feat->rows > 1 ? feat->rows : 1;
+    const double lo = feat->std_lo, hi = feat->std_hi;
+    const int ntrees = num_rounds * num_classes;
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool have = s_have != 0;
+        const double ex = s_exact;
+        for (int t = threadIdx.x; t < ntrees; t += kSelThreads) {
+            int i = int(tree_off[t]);
+            bool amb = false;
+            while (true) {
+                const DevNode nd = nodes[i];
+                if (nd.feature < 0) break;
+                const int d = decide(nd, nnz, rows, n_cols, hw, lo, hi, have, ex);
+                if (d == 2) {
+                    amb = true;
+                    break;
+                }
+                i = d ? nd.left : nd.right;
+            }
+            if (amb) atomicOr(&ambiguous, 1);
+            else leaf[t] = nodes[i].value;
+        }
+        __syncthreads();
+        if (!ambiguous) break;
+        // Rare: a std_row threshold inside the proven interval. Replay the
+        // reference's sequential sum once (features.hpp:27-35) and cache it.
+        if (threadIdx.x == 0) {
+            const double mean = feat->mean;
+            double ss = 0.0;
+            const int M = int(feat->rows);
+            int prev = rp[0];
+            for (int r = 0; r < M; ++r) {
+                const int next = rp[r + 1];
+                const double d = __dsub_rn(double(next - prev), mean);
+                ss = __dadd_rn(ss, __dmul_rn(d, d));
+                prev = next;
+            }
+            const double sd = M > 0 ? __dsqrt_rn(__ddiv_rn(ss, double(M))) : 0.0;
+            feat->std_exact = sd;
+            feat->exact_valid = 1;
+            s_exact = sd;
+            s_have = 1;
+            ambiguous = 0;
+        }
+        __syncthreads();
+    }
+    // raw_scores: per class, sum over rounds in order from 0.0 (gbdt.hpp:60-65).
+    if (threadIdx.x < num_classes) {
+        double s = 0.0;
+        for (int r = 0; r < num_rounds; ++r) s = __dadd_rn(s, leaf[r * num_classes + threadIdx.x]);
+        scores[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int c = 1; c < num_classes; ++c)
+            if (scores[c] > scores[best]) best = c;
+        *out_kernel = best;
+        if (use_cond) cudaGraphSetConditional(cond, unsigned(best));
+    }
+}
+
+uint64_t model_generation(const daspmm_model* m) { return m->generation; }
+
+int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
+                  int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s) {
+    const int ntrees = int(m->rounds.size()) * m->num_classes;
+    const size_t smem = sizeof(double) * size_t(std::max(ntrees, 1));
+    if (m->num_classes > kMaxClasses)
+        return fail(DASPMM_ERR_UNSUPPORTED, "select: more than 16 classes");
+    if (smem > 200 * 1024) return fail(DASPMM_ERR_UNSUPPORTED, "select: ensemble too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_select<<<1, kSelThreads, smem, s>>>(m->d_nodes, m->d_tree_off, int(m->rounds.size()),
+                                          m->num_classes, h->rp, h->d_feat, n_cols, hw, d_kernel,
+                                          cond, use_cond ? 1 : 0);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "select");
+}
+
+}  // namespace daspmm
+
+using namespace daspmm;
+
+extern "C" {
+
+int daspmm_model_parse(const char* text, size_t len, daspmm_model** out) {
+    if (!text || !out) return fail(DASPMM_ERR_INVALID_ARG, "model_parse: null argument");
+    *out = nullptr;
+    return parse_model(text, len, out);
+}
+
+int daspmm_model_destroy(daspmm_model* m) {
+    if (!m) return DASPMM_OK;
+    cudaFree(m->d_nodes);
+    cudaFree(m->d_tree_off);
+    delete m;
+    return DASPMM_OK;
+}
+
+int daspmm_model_info(const daspmm_model* m, int* nc, int* nf, int* nr, int* uh) {
+    if (!m) return fail(DASPMM_ERR_INVALID_ARG, "model_info: null model");
+    if (nc) *nc = m->num_classes;
+    if (nf) *nf = m->num_features;
+    if (nr) *nr = int(m->rounds.size());
+    if (uh) *uh = m->uses_hardware ? 1 : 0;
+    return DASPMM_OK;
+}
+
+int daspmm_model_predict_host(const daspmm_model* m, int64_t nnz, int64_t mat_size, double std_row,
+                              int64_t n_cols, int64_t hw, int* kernel) {
+    if (!m || !kernel) return fail(DASPMM_ERR_INVALID_ARG, "predict: null argument");
+    return predict_host(m, nnz, mat_size, std_row, n_cols, hw, kernel);
+}
+
+int daspmm_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
+                  int* d_kernel, daspmm_stream stream) {
+    if (!h || !m || !d_kernel) return fail(DASPMM_ERR_INVALID_ARG, "select: null argument");
+    if (m->uses_hardware && hw < 0)
+        return fail(DASPMM_ERR_INVALID_ARG,
+                    "encode_features: model expects a hardware_id but the sample has none");
+    if (m->num_features != (m->uses_hardware ? 5 : 4))
+        return fail(DASPMM_ERR_INVALID_ARG, "predict: feature count mismatch");
+    if (h->M == 0)
+        return fail(DASPMM_ERR_INVALID_ARG, "extract_features: matrix has no rows to summarize");
+    if (!m->d_nodes) return fail(DASPMM_ERR_CUDA, "select: model not resident on a device");
+    DeviceGuard g(h->device);
+    return launch_select(h, m, n_cols, hw, d_kernel, cudaGraphConditionalHandle{}, false,
+                         static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

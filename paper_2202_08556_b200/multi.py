@@ -1,0 +1,91 @@
+"""Multi-GPU DA-SpMM on one box: one process per GPU, torch.distributed
+for plumbing, NCCL over NVLink only where the output must be assembled.
+
+Rows of C depend only on rows of A and columns of C only on the same columns of B
+(spmm.hpp:23-30), so the path shards without any exchange:
+
+  row panels (B replicated)  rank p owns rows [cut[p], cut[p+1]) with cuts at
+                             row_of_element(A, floor(p * nnz / P)) (partition.hpp:27-30,
+                             45-64, snapped to row starts) — whole rows, ~equal nnz, no
+                             cross-GPU atomics; each rank runs the device selector on its
+                             own panel's features.
+  N-split (A replicated)     rank p owns columns [N*p/P, N*(p+1)/P) of B and C.
+
+C stays sharded by default. `gather_rows` / `gather_cols` assemble it on every rank
+with NCCL all-gather when a consumer needs the full matrix (timed separately).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def row_of_element(row_offsets: np.ndarray, e: int) -> int:
+    """partition.hpp:27-30: upper_bound(row_offsets, e) - 1."""
+    return int(np.searchsorted(row_offsets, e, side="right")) - 1
+
+
+def row_panel_cuts(row_offsets, parts: int) -> np.ndarray:
+    """nnz-balanced row cuts: cut[p] = first row whose start is >= floor(p*nnz/P)
+    snapped down to the start of the row holding that element. Returns parts+1 cuts,
+    cut[0] = 0, cut[parts] = M, nondecreasing."""
+    rp = np.asarray(row_offsets, dtype=np.int64)
+    M = rp.size - 1
+    nnz = int(rp[-1])
+    cuts = np.zeros(parts + 1, dtype=np.int64)
+    cuts[parts] = M
+    for p in range(1, parts):
+        e = (p * nnz) // parts
+        if nnz == 0:
+            cuts[p] = (p * M) // parts
+            continue
+        r = row_of_element(rp, min(e, nnz - 1))
+        cuts[p] = max(r, cuts[p - 1])
+    return cuts
+
+
+def col_split(N: int, parts: int):
+    return [(N * p) // parts for p in range(parts + 1)]
+
+
+def choose_partition(M: int, K: int, nnz: int, N: int, parts: int, elem: int = 4) -> str:
+    """Pick 'rows' or 'cols' by per-GPU compulsory bytes:
+    rows: A/P + B + C/P ; cols: A + B/P + C/P."""
+    a = 4 * (M + 1) + (4 + elem) * nnz
+    b = elem * K * N
+    c = elem * M * N
+    rows = a / parts + b + c / parts
+    cols = a + b / parts + c / parts
+    return "rows" if rows <= cols else "cols"
+
+
+def gather_rows(local_c, cuts, group=None):
+    """All-gather row panels of C (unequal sizes) into the full M x N matrix on every
+    rank: pad to the largest panel, one NCCL all-gather, then trim."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    sizes = [int(cuts[p + 1] - cuts[p]) for p in range(world)]
+    mx = max(sizes)
+    n = local_c.shape[1]
+    pad = torch.zeros(mx, n, dtype=local_c.dtype, device=local_c.device)
+    pad[: local_c.shape[0]].copy_(local_c)
+    out = torch.empty(world * mx, n, dtype=local_c.dtype, device=local_c.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return torch.cat([out[p * mx: p * mx + sizes[p]] for p in range(world)], 0)
+
+
+def gather_cols(local_c, bounds, group=None):
+    """All-gather N-split column slices into the full M x N row-major C."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    widths = [bounds[p + 1] - bounds[p] for p in range(world)]
+    mx = max(widths)
+    M = local_c.shape[0]
+    pad = torch.zeros(M, mx, dtype=local_c.dtype, device=local_c.device)
+    pad[:, : local_c.shape[1]].copy_(local_c)
+    out = torch.empty(world, M, mx, dtype=local_c.dtype, device=local_c.device)
+    dist.all_gather_into_tensor(out.view(world * M, mx), pad, group=group)
+    return torch.cat([out[p, :, : widths[p]] for p in range(world)], 1)

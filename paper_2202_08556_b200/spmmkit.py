@@ -1,0 +1,488 @@
+"""spmmkit's hot-path API (proj/include/spmmkit) over the B200 library.
+
+Same names, argument meaning and error behaviour as the reference's C++ API, so the
+parity tests read like the reference's own tests:
+
+  reference (C++)                                   here
+  ------------------------------------------------  -------------------------------------
+  CsrMatrix<T> (types.hpp:28-91)                    CsrMatrix  (host, int64 indices)
+  DenseMatrix<T>, Layout (types.hpp:16, 158-206)    DenseMatrix, Layout
+  KernelId, all_kernels (kernel_id.hpp:12-76)       KernelId, all_kernels
+  WorkerConfig, make_config (worker.hpp:18-55)      WorkerConfig, make_config, ...
+  spmm / spmm_auto_layout (spmm.hpp:194-281)        spmm / spmm_auto_layout  (run on the GPU)
+  extract_features (features.hpp:21-41)             extract_features           (GPU)
+  partition_elements (partition.hpp:45-64)          partition_elements         (GPU kernel)
+  load_selector / predict_kernel (selector.hpp)     load_selector / predict_kernel
+  —                                                 DeviceCsr: device-resident handle,
+                                                    spmm_device / select_device /
+                                                    spmm_selected (torch tensors)
+
+std::invalid_argument -> ValueError (InvalidArgument), std::out_of_range ->
+IndexError (OutOfRange), ModelFormatError -> ModelFormatError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import InvalidArgument, ModelFormatError, OutOfRange, check, lib
+
+__all__ = [
+    "Layout", "KernelId", "all_kernels", "kNumKernels", "WorkerConfig", "validate_config",
+    "is_valid", "recommended_col_block", "make_config", "CsrMatrix", "DenseMatrix",
+    "convert_layout", "DeviceCsr", "spmm", "spmm_auto_layout", "spmm_device",
+    "extract_features", "FeatureVector", "partition_elements", "SelectorModel", "load_selector",
+    "predict_kernel", "Tolerance", "tolerance_equal", "InvalidArgument", "OutOfRange",
+    "ModelFormatError",
+]
+
+
+class Layout(enum.IntEnum):
+    RowMajor = _lib.ROW_MAJOR
+    ColMajor = _lib.COL_MAJOR
+
+
+# ------------------------------------------------------------------ kernel_id.hpp
+_M = ("RB", "EB")
+_N = ("RM", "CM")
+_K = ("SR", "PR")
+kNumKernels = 8
+
+
+@dataclass(frozen=True)
+class KernelId:
+    """One point of the 2x2x2 design space; index = 4m + 2n + k (kernel_id.hpp:25-27)."""
+    m: int = 0
+    n: int = 0
+    k: int = 0
+
+    def index(self) -> int:
+        return self.m * 4 + self.n * 2 + self.k
+
+    @staticmethod
+    def from_index(idx: int) -> "KernelId":
+        if idx < 0 or idx > 7:
+            raise OutOfRange(_lib.ERR_OUT_OF_RANGE, "KernelId index must be 0..7")
+        return KernelId(idx // 4, (idx // 2) % 2, idx % 2)
+
+    def name(self) -> str:
+        return f"{_M[self.m]}+{_N[self.n]}+{_K[self.k]}"
+
+    @staticmethod
+    def parse(s: str) -> Optional["KernelId"]:
+        if len(s) != 8 or s[2] != "+" or s[5] != "+":
+            return None
+        try:
+            return KernelId(_M.index(s[0:2]), _N.index(s[3:5]), _K.index(s[6:8]))
+        except ValueError:
+            return None
+
+    def __int__(self):
+        return self.index()
+
+    def __repr__(self):
+        return f"KernelId({self.name()})"
+
+
+def all_kernels():
+    return [KernelId.from_index(i) for i in range(kNumKernels)]
+
+
+# ------------------------------------------------------------------ worker.hpp
+@dataclass
+class WorkerConfig:
+    num_workers: int = 1  # P
+    group_width: int = 8  # W
+    col_block: int = 4    # C
+
+
+def validate_config(cfg: WorkerConfig):
+    """worker.hpp:29-40 — list of issues, empty when valid."""
+    issues = []
+    if cfg.num_workers < 1:
+        issues.append(f"num_workers must be >= 1, got {cfg.num_workers}")
+    w = cfg.group_width
+    if w < 2 or (w & (w - 1)) != 0:
+        issues.append(f"group_width must be a power of two >= 2, got {w}")
+    if cfg.col_block < 1:
+        issues.append(f"col_block must be >= 1, got {cfg.col_block}")
+    return issues
+
+
+def is_valid(cfg: WorkerConfig) -> bool:
+    return not validate_config(cfg)
+
+
+def recommended_col_block(kernel: KernelId, n_cols: int) -> int:
+    """worker.hpp:47-50."""
+    cap = 4 if kernel.k == 1 else 8
+    return max(1, min(n_cols, cap))
+
+
+def make_config(kernel: KernelId, n_cols: int, num_workers: int = 1, group_width: int = 8):
+    return WorkerConfig(num_workers, group_width, recommended_col_block(kernel, n_cols))
+
+
+# ------------------------------------------------------------------ types.hpp
+class CsrMatrix:
+    """Host CSR with int64 offsets/indices (types.hpp:28-35)."""
+
+    def __init__(self, num_rows=0, num_cols=0, row_offsets=None, col_indices=None, values=None,
+                 dtype=np.float64):
+        self.num_rows = int(num_rows)
+        self.num_cols = int(num_cols)
+        self.row_offsets = np.zeros(1, np.int64) if row_offsets is None else \
+            np.ascontiguousarray(row_offsets, np.int64)
+        self.col_indices = np.zeros(0, np.int64) if col_indices is None else \
+            np.ascontiguousarray(col_indices, np.int64)
+        self.values = np.zeros(0, dtype) if values is None else np.ascontiguousarray(values, dtype)
+
+    def nnz(self) -> int:
+        return int(self.col_indices.size)
+
+    def row_nnz(self, m: int) -> int:
+        return int(self.row_offsets[m + 1] - self.row_offsets[m])
+
+    @staticmethod
+    def identity(n: int, dtype=np.float64) -> "CsrMatrix":
+        return CsrMatrix(n, n, np.arange(n + 1), np.arange(n), np.ones(n, dtype), dtype)
+
+    @staticmethod
+    def from_coo(num_rows, num_cols, triplets, dtype=np.float64) -> "CsrMatrix":
+        """types.hpp:56-90: sort by (row, col), sum duplicates."""
+        if len(triplets) == 0:
+            return CsrMatrix(num_rows, num_cols, np.zeros(num_rows + 1, np.int64), None, None, dtype)
+        r = np.array([t[0] for t in triplets], np.int64)
+        c = np.array([t[1] for t in triplets], np.int64)
+        v = np.array([t[2] for t in triplets], dtype)
+        if (r < 0).any() or (r >= num_rows).any() or (c < 0).any() or (c >= num_cols).any():
+            raise InvalidArgument(_lib.ERR_INVALID_ARG, "from_coo: coordinate out of bounds")
+        order = np.lexsort((c, r))
+        r, c, v = r[order], c[order], v[order]
+        keep = np.ones(r.size, bool)
+        keep[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        grp = np.cumsum(keep) - 1
+        vs = np.zeros(int(keep.sum()), dtype)
+        # duplicates summed in sorted order, left to right (types.hpp:67-80)
+        for i in range(v.size):
+            vs[grp[i]] = vs[grp[i]] + v[i] if not keep[i] else v[i]
+        r, c = r[keep], c[keep]
+        rp = np.zeros(num_rows + 1, np.int64)
+        np.add.at(rp, r + 1, 1)
+        return CsrMatrix(num_rows, num_cols, np.cumsum(rp), c, vs, dtype)
+
+    def astype(self, dtype) -> "CsrMatrix":
+        return CsrMatrix(self.num_rows, self.num_cols, self.row_offsets, self.col_indices,
+                         self.values.astype(dtype), dtype)
+
+
+class DenseMatrix:
+    """Dense operand with explicit layout (types.hpp:158-194). ``data`` is the flat
+    buffer in memory order, as the reference's std::vector."""
+
+    def __init__(self, rows, cols, layout=Layout.RowMajor, data=None, dtype=np.float64):
+        self.num_rows = int(rows)
+        self.num_cols = int(cols)
+        self.layout = Layout(layout)
+        self.data = np.zeros(self.num_rows * self.num_cols, dtype) if data is None else \
+            np.ascontiguousarray(data, dtype).reshape(-1)
+
+    @property
+    def dtype(self):
+        return self.data.dtype
+
+    def index_of(self, r, c):
+        return r * self.num_cols + c if self.layout == Layout.RowMajor else c * self.num_rows + r
+
+    def at(self, r, c):
+        return self.data[self.index_of(r, c)]
+
+    def logical(self) -> np.ndarray:
+        """rows x cols array in logical order."""
+        if self.layout == Layout.RowMajor:
+            return self.data.reshape(self.num_rows, self.num_cols)
+        return self.data.reshape(self.num_cols, self.num_rows).T
+
+    @staticmethod
+    def from_logical(a: np.ndarray, layout=Layout.RowMajor) -> "DenseMatrix":
+        a = np.asarray(a)
+        buf = a if layout == Layout.RowMajor else a.T
+        return DenseMatrix(a.shape[0], a.shape[1], layout, np.ascontiguousarray(buf).reshape(-1),
+                           a.dtype)
+
+    @staticmethod
+    def zeros(rows, cols, layout=Layout.RowMajor, dtype=np.float64):
+        return DenseMatrix(rows, cols, layout, None, dtype)
+
+
+def convert_layout(m: DenseMatrix, target: Layout) -> DenseMatrix:
+    """types.hpp:198-206."""
+    if m.layout == target:
+        return DenseMatrix(m.num_rows, m.num_cols, m.layout, m.data.copy(), m.dtype)
+    return DenseMatrix.from_logical(m.logical(), target)
+
+
+# ------------------------------------------------------------------ device handle
+def _dtype_code(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return _lib.F32
+    if dt == np.float64:
+        return _lib.F64
+    raise InvalidArgument(_lib.ERR_INVALID_ARG, f"unsupported value type {dt}")
+
+
+class DeviceCsr:
+    """Device-resident CSR handle (int32 offsets/cols on the GPU)."""
+
+    def __init__(self, handle: int, dtype, keepalive=None):
+        self._h = C.c_void_p(handle)
+        self.dtype = np.dtype(dtype)
+        self._keep = keepalive
+        M, K, nnz, dt, ne, ct = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int(), C.c_int64(),
+                                 C.c_int64())
+        check(lib().daspmm_csr_info(self._h, C.byref(M), C.byref(K), C.byref(nnz), C.byref(dt),
+                                    C.byref(ne), C.byref(ct)))
+        self.num_rows, self.num_cols, self._nnz = M.value, K.value, nnz.value
+        self.empty_rows, self.cols_touched = ne.value, ct.value
+
+    @staticmethod
+    def from_host(a: CsrMatrix, dtype=None) -> "DeviceCsr":
+        dtype = np.dtype(dtype or a.values.dtype)
+        vals = np.ascontiguousarray(a.values, dtype)
+        rp = np.ascontiguousarray(a.row_offsets, np.int64)
+        ci = np.ascontiguousarray(a.col_indices, np.int64)
+        out = C.c_void_p()
+        check(lib().daspmm_csr_create_host(a.num_rows, a.num_cols, a.nnz(), rp.ctypes.data,
+                                           ci.ctypes.data, vals.ctypes.data, _dtype_code(dtype),
+                                           C.byref(out)))
+        return DeviceCsr(out.value, dtype)
+
+    @staticmethod
+    def from_device(num_rows, num_cols, row_offsets, col_indices, values, copy=False,
+                    stream=None) -> "DeviceCsr":
+        """torch int32 offsets/cols and float32/float64 values on the GPU."""
+        import torch
+
+        assert row_offsets.dtype == torch.int32 and col_indices.dtype == torch.int32
+        dtype = np.float32 if values.dtype == torch.float32 else np.float64
+        out = C.c_void_p()
+        check(lib().daspmm_csr_create_device(num_rows, num_cols, col_indices.numel(),
+                                             row_offsets.data_ptr(), col_indices.data_ptr(),
+                                             values.data_ptr(), _dtype_code(dtype), int(copy),
+                                             _stream_ptr(stream), C.byref(out)))
+        keep = None if copy else (row_offsets, col_indices, values)
+        return DeviceCsr(out.value, dtype, keep)
+
+    def panel(self, r0: int, r1: int, stream=None) -> "DeviceCsr":
+        out = C.c_void_p()
+        check(lib().daspmm_csr_create_panel(self._h, r0, r1, _stream_ptr(stream), C.byref(out)))
+        return DeviceCsr(out.value, self.dtype)
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    def device_arrays(self):
+        rp, ci, va = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().daspmm_csr_device_arrays(self._h, C.byref(rp), C.byref(ci), C.byref(va)))
+        return rp.value, ci.value, va.value
+
+    def close(self):
+        if self._h:
+            lib().daspmm_csr_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _as_device(a) -> DeviceCsr:
+    return a if isinstance(a, DeviceCsr) else DeviceCsr.from_host(a)
+
+
+# ------------------------------------------------------------------ spmm.hpp
+def spmm(kernel: KernelId, a, x: DenseMatrix, cfg: WorkerConfig, exact: bool = False) -> DenseMatrix:
+    """spmm() — spmm.hpp:194-271, computed on the GPU. Same checks and messages:
+    config, then dimensions, then layout. Returns a RowMajor DenseMatrix.
+
+    ``exact`` selects the reference evaluation order (bit-identical results; EB
+    honours cfg.num_workers as the chunk count). Otherwise the library fuses
+    multiply-adds and picks the EB chunking itself (tolerance parity)."""
+    issues = validate_config(cfg)
+    if issues:
+        raise InvalidArgument(_lib.ERR_INVALID_CONFIG, "spmm: invalid config; " + "; ".join(issues))
+    if a.num_cols != x.num_rows:
+        raise InvalidArgument(_lib.ERR_DIMS, f"spmm: A is {a.num_rows}x{a.num_cols} but X has "
+                                              f"{x.num_rows} rows")
+    want = Layout.ColMajor if kernel.n == 1 else Layout.RowMajor
+    if x.layout != want:
+        raise InvalidArgument(_lib.ERR_LAYOUT, f"spmm: kernel {kernel.name()} needs {want.name} X, "
+                                                f"got {x.layout.name}")
+    d = _as_device(a)
+    if d.dtype != x.dtype:
+        raise InvalidArgument(_lib.ERR_INVALID_ARG, "spmm: A and X value types differ")
+    n = x.num_cols
+    y = np.zeros(a.num_rows * n, x.dtype)
+    P = cfg.num_workers if exact else 0
+    xb = np.ascontiguousarray(x.data)
+    check(lib().daspmm_spmm_host(d._h, kernel.index(), P, cfg.group_width, cfg.col_block,
+                                 xb.ctypes.data, int(x.layout), n, y.ctypes.data,
+                                 _lib.EXACT if exact else 0))
+    return DenseMatrix(a.num_rows, n, Layout.RowMajor, y, x.dtype)
+
+
+def spmm_auto_layout(kernel: KernelId, a, x: DenseMatrix, cfg: WorkerConfig,
+                     exact: bool = False) -> DenseMatrix:
+    """spmm.hpp:275-281."""
+    want = Layout.ColMajor if kernel.n == 1 else Layout.RowMajor
+    return spmm(kernel, a, x if x.layout == want else convert_layout(x, want), cfg, exact)
+
+
+def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int = 4,
+                b_layout: Layout = None, exact: bool = False, stream=None):
+    """Device-operand SpMM on torch tensors. B: K x N row-major tensor, or — for
+    b_layout=ColMajor — an N x K tensor (the column-major buffer). C_out: M x N."""
+    kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
+    if b_layout is None:
+        b_layout = Layout.ColMajor if (kid >> 1) & 1 else Layout.RowMajor
+    if b_layout == Layout.RowMajor:
+        n, ldb = B.shape[1], B.stride(0)
+    else:
+        n, ldb = B.shape[0], B.stride(0)
+    check(lib().daspmm_spmm(a._h, kid, P, W, Cb, B.data_ptr(), int(b_layout), ldb, n,
+                            C_out.data_ptr(), C_out.stride(0), _lib.EXACT if exact else 0,
+                            _stream_ptr(stream)))
+    return C_out
+
+
+# ------------------------------------------------------------------ features / partition
+@dataclass
+class FeatureVector:
+    nnz: int = 0
+    mat_size: int = 0
+    std_row: float = 0.0
+    n_cols: int = 0
+    hardware_id: Optional[int] = None
+
+
+def extract_features(a, n_cols: int, hardware_id: Optional[int] = None) -> FeatureVector:
+    """features.hpp:21-41, on the device (std_row bit-identical to the reference)."""
+    if a.num_rows == 0:
+        raise InvalidArgument(_lib.ERR_INVALID_ARG,
+                              "extract_features: matrix has no rows to summarize")
+    d = _as_device(a)
+    nnz, ms, sd = C.c_int64(), C.c_int64(), C.c_double()
+    check(lib().daspmm_extract_features(d._h, n_cols, C.byref(nnz), C.byref(ms), C.byref(sd)))
+    return FeatureVector(nnz.value, ms.value, sd.value, n_cols, hardware_id)
+
+
+def partition_elements(a, p: int):
+    """partition.hpp:45-64 via the device partition kernel. Returns
+    (begin, end, row_of_chunk_start) int64 arrays."""
+    if p < 1:
+        raise InvalidArgument(_lib.ERR_INVALID_ARG, "partition_elements: need p >= 1")
+    d = _as_device(a)
+    b = np.zeros(p, np.int64)
+    e = np.zeros(p, np.int64)
+    r = np.zeros(p, np.int64)
+    check(lib().daspmm_partition(d._h, p, b.ctypes.data, e.ctypes.data, r.ctypes.data))
+    return b, e, r
+
+
+# ------------------------------------------------------------------ selector
+class SelectorModel:
+    """load_selector result (selector.hpp:12-15, 119-132)."""
+
+    def __init__(self, text: str):
+        raw = text.encode()
+        self._m = C.c_void_p()
+        check(lib().daspmm_model_parse(raw, len(raw), C.byref(self._m)))
+        nc, nf, nr, uh = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(lib().daspmm_model_info(self._m, C.byref(nc), C.byref(nf), C.byref(nr), C.byref(uh)))
+        self.num_classes, self.num_features, self.num_rounds = nc.value, nf.value, nr.value
+        self.uses_hardware = bool(uh.value)
+
+    def close(self):
+        if self._m:
+            lib().daspmm_model_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def load_selector(text_or_stream) -> SelectorModel:
+    text = text_or_stream if isinstance(text_or_stream, str) else text_or_stream.read()
+    return SelectorModel(text)
+
+
+def predict_kernel(model: SelectorModel, f: FeatureVector) -> KernelId:
+    """selector.hpp:62-65 (host evaluation in the reference's arithmetic)."""
+    k = C.c_int()
+    hw = -1 if f.hardware_id is None else int(f.hardware_id)
+    check(lib().daspmm_model_predict_host(model._m, f.nnz, f.mat_size, f.std_row, f.n_cols, hw,
+                                          C.byref(k)))
+    return KernelId.from_index(k.value)
+
+
+def select_device(a: DeviceCsr, model: SelectorModel, n_cols: int, out, hw: int = -1,
+                  stream=None):
+    """Device selector: writes the kernel id into ``out`` (torch int32 on the GPU)."""
+    check(lib().daspmm_select(a._h, model._m, n_cols, hw, out.data_ptr(), _stream_ptr(stream)))
+    return out
+
+
+def spmm_selected(a: DeviceCsr, model: SelectorModel, B, C_out, b_layout=Layout.RowMajor,
+                  W: int = 8, hw: int = -1, exact: bool = False, kernel_out=None, stream=None):
+    """DA-SpMM: device selector + on-device dispatch (graph SWITCH node)."""
+    if b_layout == Layout.RowMajor:
+        n, ldb = B.shape[1], B.stride(0)
+    else:
+        n, ldb = B.shape[0], B.stride(0)
+    kp = kernel_out.data_ptr() if kernel_out is not None else None
+    check(lib().daspmm_spmm_selected(a._h, model._m, hw, B.data_ptr(), int(b_layout), ldb, n,
+                                     C_out.data_ptr(), C_out.stride(0), W,
+                                     _lib.EXACT if exact else 0, kp, _stream_ptr(stream)))
+    return C_out
+
+
+# ------------------------------------------------------------------ tolerance
+class Tolerance:
+    """spmm.hpp:283-295."""
+    rtol = {np.dtype(np.float64): 1e-10, np.dtype(np.float32): 1e-3}
+    atol = {np.dtype(np.float64): 1e-12, np.dtype(np.float32): 1e-6}
+
+
+def tolerance_equal(y: DenseMatrix, ref: DenseMatrix, rtol=None, atol=None) -> bool:
+    """spmm.hpp:298-309."""
+    if y.num_rows != ref.num_rows or y.num_cols != ref.num_cols:
+        return False
+    rtol = Tolerance.rtol[y.dtype] if rtol is None else rtol
+    atol = Tolerance.atol[y.dtype] if atol is None else atol
+    a = y.logical().astype(np.float64)
+    b = ref.logical().astype(np.float64)
+    return bool(np.all(np.abs(a - b) <= atol + rtol * np.abs(b)))

@@ -1,0 +1,290 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the reference.
+
+Modelled on the reference's own suites (tests/test_spmm.cpp, acceptance_test.cpp C1/C2/C8):
+  * exact mode (DASPMM_EXACT, P honoured) is bit-identical to the reference's spmm()
+    for every RB kernel, and for every EB row owned by a single chunk; EB rows shared
+    by chunks (atomic deposits in both implementations) are held to Tolerance<T>;
+  * fast mode (FFMA, library-chosen chunking) is held to the order-independent bound
+    |y - y64| <= 2*gamma(len+1)*sum|a*x| against the fp64 oracle, and to
+    the reference's own Tolerance<float> (rtol 1e-3, atol 1e-6) against spmm_reference<float>.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+import helpers as H  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2202_08556_b200 import spmmkit
+
+    spmmkit.lib()
+    return spmmkit
+
+
+def _case(sk, z, meta, name, dtype):
+    m = meta["cases"][name]
+    return sk.CsrMatrix(m["rows"], m["cols"], z[f"{name}/rp"], z[f"{name}/ci"],
+                        z[f"{name}/va"].astype(dtype), dtype)
+
+
+@pytest.mark.parametrize("dt", ["64", "32"])
+def test_exact_mode_matches_reference_golden(sk, golden, golden_meta, dt):
+    dtype = np.float64 if dt == "64" else np.float32
+    n_checked = 0
+    for name in sorted(golden_meta["cases"]):
+        a = _case(sk, golden, golden_meta, name, dtype)
+        d = sk.DeviceCsr.from_host(a)
+        for n in golden_meta["cases"][name]["ns"]:
+            x = golden[f"{name}/n{n}/x{dt}"]
+            for k in range(8):
+                kid = sk.KernelId.from_index(k)
+                for (P, W, Cb) in golden_meta["cases"][name]["configs"]:
+                    if W > 32:
+                        continue
+                    want = golden[f"{name}/n{n}/k{k}/P{P}W{W}C{Cb}/y{dt}"]
+                    xd = sk.DenseMatrix.from_logical(x, sk.Layout.ColMajor if k & 2 else
+                                                     sk.Layout.RowMajor)
+                    y = sk.spmm(kid, d, xd, sk.WorkerConfig(P, W, Cb), exact=True).logical()
+                    if k < 4:
+                        np.testing.assert_array_equal(y, want, err_msg=f"{name} {kid} P{P}W{W}")
+                    else:
+                        shared = H.split_rows(a, P)
+                        np.testing.assert_array_equal(y[~shared], want[~shared],
+                                                      err_msg=f"{name} {kid} P{P}W{W}")
+                        rt = 1e-10 if dt == "64" else 1e-3
+                        np.testing.assert_allclose(y, want, rtol=rt, atol=rt)
+                    n_checked += 1
+    assert n_checked > 400
+
+
+@pytest.mark.parametrize("dt", ["64", "32"])
+def test_fast_mode_within_gamma_bound(sk, golden, golden_meta, dt):
+    dtype = np.float64 if dt == "64" else np.float32
+    for name in sorted(golden_meta["cases"]):
+        a = _case(sk, golden, golden_meta, name, dtype)
+        d = sk.DeviceCsr.from_host(a)
+        for n in golden_meta["cases"][name]["ns"]:
+            x = golden[f"{name}/n{n}/x{dt}"]
+            y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+            bound = H.gamma_bound(a, x, dtype)
+            ref32 = golden[f"{name}/n{n}/ref{dt}"]
+            for k in range(8):
+                kid = sk.KernelId.from_index(k)
+                for W in (2, 8, 32):
+                    y = sk.spmm_auto_layout(kid, d, sk.DenseMatrix.from_logical(x),
+                                            sk.WorkerConfig(1, W, 4)).logical()
+                    err = np.abs(y.astype(np.float64) - y64)
+                    assert (err <= bound).all(), f"{name} {kid} W{W} n{n}: {err.max()}"
+                    assert sk.tolerance_equal(sk.DenseMatrix.from_logical(y),
+                                              sk.DenseMatrix.from_logical(ref32)), f"{name} {kid}"
+
+
+@pytest.mark.parametrize("skew", [0.0, 1.2])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 16, 32, 33, 64, 128, 256])
+def test_random_matrices_all_kernels(sk, n, skew):
+    """test_spmm.cpp:99-126 style, larger: random/power-law rows incl. very long rows."""
+    rng = np.random.default_rng(100 + n)
+    a = H.random_csr(3000, 2500, 60000, seed=n, dtype=np.float32, skew=skew)
+    x = rng.uniform(-1, 1, (2500, n)).astype(np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+    bound = H.gamma_bound(a, x, np.float32)
+    for k in range(8):
+        for W in (4, 32):
+            kid = sk.KernelId.from_index(k)
+            y = sk.spmm_auto_layout(kid, d, sk.DenseMatrix.from_logical(x),
+                                    sk.WorkerConfig(1, W, 4)).logical()
+            err = np.abs(y.astype(np.float64) - y64)
+            assert (err <= bound).all(), f"{kid} W{W} n{n}: max err {err.max()}"
+
+
+def test_rb_sr_bit_identical_to_spmm_reference_float(sk):
+    """RB+RM+SR and RB+CM+SR equal spmm_reference<float> bit for bit
+    (exact mode), at N = 2 / 32 / 128."""
+    a = H.random_csr(2000, 1500, 40000, seed=9, dtype=np.float32, skew=1.0)
+    d = sk.DeviceCsr.from_host(a)
+    for n in (2, 32, 128):
+        x = np.random.default_rng(n).uniform(-1, 1, (1500, n)).astype(np.float32)
+        ref = O.spmm_reference(H.to_oracle(a).__class__(a.num_rows, a.num_cols, a.row_offsets,
+                                                         a.col_indices, a.values), x,
+                               dtype=np.float32)
+        for k in (0, 2):
+            y = sk.spmm_auto_layout(sk.KernelId.from_index(k), d, sk.DenseMatrix.from_logical(x),
+                                    sk.WorkerConfig(1, 8, 4), exact=True).logical()
+            np.testing.assert_array_equal(y, ref)
+
+
+def test_rb_pr_bit_identical_to_oracle_kernel(sk):
+    """RB+PR exact mode == reference RB+PR (adjacent tree) at equal W, float."""
+    a = H.random_csr(500, 400, 9000, seed=3, dtype=np.float32, skew=1.1)
+    d = sk.DeviceCsr.from_host(a)
+    x = np.random.default_rng(1).uniform(-1, 1, (400, 12)).astype(np.float32)
+    for W in (2, 4, 8, 16, 32):
+        for k in (1, 3):
+            want = O.spmm_kernel(k, H.to_oracle(a), x, 3, W, 4, dtype=np.float32)
+            y = sk.spmm_auto_layout(sk.KernelId.from_index(k), d, sk.DenseMatrix.from_logical(x),
+                                    sk.WorkerConfig(3, W, 4), exact=True).logical()
+            np.testing.assert_array_equal(y, want, err_msg=f"k{k} W{W}")
+
+
+def test_eb_exact_matches_oracle_on_owned_rows(sk):
+    a = H.random_csr(800, 600, 20000, seed=5, dtype=np.float32, skew=1.3)
+    d = sk.DeviceCsr.from_host(a)
+    x = np.random.default_rng(2).uniform(-1, 1, (600, 7)).astype(np.float32)
+    for P in (1, 3, 64, 1000):
+        shared = H.split_rows(a, P)
+        for k in (4, 5, 6, 7):
+            for W in (4, 32):
+                want = O.spmm_kernel(k, H.to_oracle(a), x, P, W, 4, dtype=np.float32)
+                y = sk.spmm_auto_layout(sk.KernelId.from_index(k), d,
+                                        sk.DenseMatrix.from_logical(x), sk.WorkerConfig(P, W, 4),
+                                        exact=True).logical()
+                np.testing.assert_array_equal(y[~shared], want[~shared], err_msg=f"k{k} P{P} W{W}")
+                np.testing.assert_allclose(y, want, rtol=1e-4, atol=1e-4)
+
+
+def test_rb_deterministic_across_runs_and_workers(sk):
+    """test_spmm.cpp:163-180: RB bits independent of run and of P."""
+    a = H.random_csr(300, 200, 2500, seed=31, dtype=np.float64)
+    d = sk.DeviceCsr.from_host(a)
+    x = sk.DenseMatrix.from_logical(np.random.default_rng(32).uniform(-1, 1, (200, 5)))
+    for k in range(4):
+        kid = sk.KernelId.from_index(k)
+        first = sk.spmm_auto_layout(kid, d, x, sk.WorkerConfig(3, 4, 2)).data
+        for p in (1, 2, 7):
+            again = sk.spmm_auto_layout(kid, d, x, sk.WorkerConfig(p, 4, 2)).data
+            np.testing.assert_array_equal(again, first)
+
+
+def test_errors_match_reference(sk):
+    """test_spmm.cpp:197-224 — same exception kinds and message prefixes."""
+    a = H.csr_from_counts([6, 2, 0, 3, 1], 8)
+    x_rm = sk.DenseMatrix.from_logical(np.ones((8, 2)))
+    x_cm = sk.convert_layout(x_rm, sk.Layout.ColMajor)
+    with pytest.raises(ValueError, match="needs ColMajor X, got RowMajor"):
+        sk.spmm(sk.KernelId.parse("RB+CM+SR"), a, x_rm, sk.WorkerConfig(1, 4, 2))
+    with pytest.raises(ValueError, match="needs RowMajor X"):
+        sk.spmm(sk.KernelId.parse("EB+RM+PR"), a, x_cm, sk.WorkerConfig(1, 4, 2))
+    with pytest.raises(ValueError, match="A is 5x8 but X has 7 rows"):
+        sk.spmm(sk.KernelId.from_index(0), a, sk.DenseMatrix.from_logical(np.ones((7, 2))),
+                sk.WorkerConfig(1, 4, 2))
+    for cfg in (sk.WorkerConfig(0, 4, 2), sk.WorkerConfig(1, 3, 2), sk.WorkerConfig(1, 4, 0)):
+        with pytest.raises(ValueError, match="spmm: invalid config"):
+            sk.spmm(sk.KernelId.from_index(0), a, x_rm, cfg)
+    with pytest.raises(IndexError):
+        sk.KernelId.from_index(8)
+    # C-ABI-level checks (the ABI validates on its own, no shim in between)
+    from paper_2202_08556_b200 import _lib
+
+    import torch
+    d = sk.DeviceCsr.from_host(a)
+    B = torch.ones(8, 2, device="cuda", dtype=torch.float64)
+    Cc = torch.zeros(5, 2, device="cuda", dtype=torch.float64)
+    with pytest.raises(_lib.InvalidArgument, match="needs ColMajor"):
+        sk.spmm_device(2, d, B, Cc, b_layout=sk.Layout.RowMajor)
+    with pytest.raises(_lib.InvalidArgument, match="group_width"):
+        sk.spmm_device(1, d, B, Cc, W=6)
+
+
+def test_zero_matrix_and_zero_columns(sk):
+    """test_spmm.cpp:226-242."""
+    a = H.csr_from_counts([0, 0, 0], 4)
+    x = sk.DenseMatrix.from_logical(np.random.default_rng(3).uniform(-1, 1, (4, 3)))
+    for kid in sk.all_kernels():
+        y = sk.spmm_auto_layout(kid, a, x, sk.WorkerConfig(2, 4, 2))
+        assert (y.data == 0).all()
+    b = H.csr_from_counts([6, 2, 0, 3, 1], 8)
+    x0 = sk.DenseMatrix.zeros(8, 0)
+    for kid in sk.all_kernels():
+        y = sk.spmm_auto_layout(kid, b, x0, sk.WorkerConfig(2, 4, 2))
+        assert y.num_rows == 5 and y.num_cols == 0
+
+
+def test_identity_exact_for_all_kernels(sk):
+    """test_spmm.cpp:71-81."""
+    a = sk.CsrMatrix.identity(8)
+    x = sk.DenseMatrix.from_logical(np.random.default_rng(11).uniform(-1, 1, (8, 4)))
+    for kid in sk.all_kernels():
+        for p in (1, 2):
+            y = sk.spmm_auto_layout(kid, a, x, sk.WorkerConfig(p, 4, 2))
+            np.testing.assert_array_equal(y.logical(), x.logical())
+
+
+def test_output_fully_overwritten(sk):
+    """C is poisoned before the call; every element must be written (empty rows,
+    split rows, all kernels, fast mode)."""
+    import torch
+
+    a = H.random_csr(4000, 3000, 50000, seed=77, dtype=np.float32, skew=1.5)
+    d = sk.DeviceCsr.from_host(a)
+    x = np.random.default_rng(4).uniform(-1, 1, (3000, 16)).astype(np.float32)
+    y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+    bound = H.gamma_bound(a, x, np.float32)
+    for k in range(8):
+        B = torch.from_numpy(np.ascontiguousarray(x.T if k & 2 else x)).cuda()
+        Cc = torch.full((4000, 16), float("nan"), device="cuda")
+        sk.spmm_device(k, d, B, Cc)
+        torch.cuda.synchronize()
+        y = Cc.cpu().numpy().astype(np.float64)
+        assert np.isfinite(y).all(), k
+        assert (np.abs(y - y64) <= bound).all(), k
+
+
+def test_device_partition_matches_reference(sk, golden, golden_meta):
+    for name in sorted(golden_meta["cases"]):
+        a = _case(sk, golden, golden_meta, name, np.float64)
+        for p in (1, 2, 3, 5, 8, 64):
+            b, e, r = sk.partition_elements(a, p)
+            np.testing.assert_array_equal(np.stack([b, e, r]), golden[f"{name}/part{p}"])
+
+
+def test_device_features_bit_exact(sk, golden, golden_meta):
+    for name in sorted(golden_meta["cases"]):
+        a = _case(sk, golden, golden_meta, name, np.float64)
+        if a.num_rows == 0:
+            continue
+        f = sk.extract_features(a, 16)
+        assert f.std_row == golden[f"{name}/std_row"][0], name
+        assert f.nnz == a.nnz() and f.mat_size == a.num_rows
+    big = H.random_csr(200000, 1000, 3000000, seed=1, skew=1.4)
+    f = sk.extract_features(big, 8)
+    assert f.std_row == O.extract_features(H.to_oracle(big))[2]
+
+
+def test_device_warp_primitives_bit_exact(sk, golden):
+    import ctypes as C
+
+    from paper_2202_08556_b200 import _lib
+
+    L = _lib.lib()
+    vals, widths, sums = golden["tree/values"], golden["tree/widths"], golden["tree/sums"]
+    off = 0
+    for w, s in zip(widths, sums):
+        v = np.ascontiguousarray(vals[off:off + w])
+        off += w
+        if w > 32:
+            continue
+        out = np.zeros(1)
+        _lib.check(L.daspmm_debug_tree_reduce_f64(v.ctypes.data, int(w), out.ctypes.data))
+        assert out[0] == s
+    ids, vals, widths = golden["cond/ids"], golden["cond/values"], golden["cond/widths"]
+    seg_sums, counts = golden["cond/seg_sums"], golden["cond/counts"]
+    off = soff = 0
+    for w, cnt in zip(widths, counts):
+        v = np.ascontiguousarray(vals[off:off + w])
+        idw = np.ascontiguousarray(ids[off:off + w])
+        out = np.zeros(w)
+        _lib.check(L.daspmm_debug_conditional_scan_f64(v.ctypes.data, idw.ctypes.data, int(w),
+                                                       out.ctypes.data))
+        starts = [i for i in range(w) if i == 0 or idw[i] != idw[i - 1]]
+        assert list(out[starts]) == list(seg_sums[soff:soff + cnt])
+        off += w
+        soff += cnt
