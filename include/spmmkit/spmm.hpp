@@ -1,0 +1,4 @@
+// Forwarding header: spmmkit/spmm.hpp of the reference API (proj/include/spmmkit),
+// served by the B200 implementation in b200.hpp.
+#pragma once
+#include "spmmkit/b200.hpp"
