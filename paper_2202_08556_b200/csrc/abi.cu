@@ -14,13 +14,19 @@ namespace daspmm {
 
 static thread_local std::string g_err;
 
+static bool debug_on() {
+    static const bool on = getenv("DASPMM_DEBUG") != nullptr;
+    return on;
+}
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(int code, const std::string& msg) {
     g_err = msg;
+    if (debug_on()) fprintf(stderr, "[daspmm] error %d: %s\n", code, msg.c_str());
     return code;
 }
 int cuda_fail(cudaError_t e, const char* what) {
     g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    if (debug_on()) fprintf(stderr, "[daspmm] cuda error: %s\n", g_err.c_str());
     return DASPMM_ERR_CUDA;
 }
 
@@ -204,7 +210,7 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
                 int64_t ldb, int64_t N, void* C, int64_t ldc, unsigned flags, cudaStream_t s,
                 int* chunk_scratch) {
     if (h->M == 0 || N == 0) return DASPMM_OK;
-    keep_pool_warm(h->device);
+    if (chunk_scratch == nullptr) keep_pool_warm(h->device);  // never inside a graph capture
     const bool exact = (flags & DASPMM_EXACT) != 0;
     const Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
     int* chunk_row = chunk_scratch;

@@ -44,7 +44,9 @@ struct Entry {
     int* chunk_row = nullptr;
     void* bt = nullptr;       // B in the other layout (may be null: see twin fallback)
     int* own_kernel = nullptr;
+    int* decision = nullptr;  // device cache of the selector's choice (-1 = not yet made)
     ~Entry() {
+        cudaFree(decision);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         cudaFree(chunk_row);
@@ -93,6 +95,10 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     const int64_t ldt = k.b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
                                                        : std::max<int64_t>(k.N, 1);
 
+    if ((e = cudaMalloc(&en.decision, sizeof(int))) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaMalloc(decision)");
+    if ((e = cudaMemset(en.decision, 0xff, sizeof(int))) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaMemset(decision)");
     cudaStream_t cap;
     if ((e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking)) != cudaSuccess)
         return cuda_fail(e, "graph: stream");
@@ -110,7 +116,7 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     if ((e = cudaStreamBeginCaptureToGraph(cap, en.graph, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return cuda_fail(e, "graph: capture(select)");
-    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap);
+    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap, en.decision);
     cudaGraph_t g_out = nullptr;
     e = cudaStreamEndCapture(cap, &g_out);
     if (rc) return rc;
@@ -202,7 +208,11 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
         auto it = cache->entries.find(key);
         if (it == cache->entries.end()) {
             auto fresh = std::make_unique<Entry>();
-            if (int rc = build_entry(h, m, key, *fresh)) return rc;
+            if (int rc = build_entry(h, m, key, *fresh)) {
+                // A graph left mid-capture cannot be destroyed safely; leak it.
+                fresh->graph = nullptr;
+                return rc;
+            }
             it = cache->entries.emplace(key, std::move(fresh)).first;
         }
         en = it->second.get();

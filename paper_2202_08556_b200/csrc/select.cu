@@ -275,8 +275,21 @@ __device__ __forceinline__ int decide(const DevNode& nd, long long f0, long long
 __global__ void __launch_bounds__(kSelThreads)
 k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off, int num_rounds,
          int num_classes, const int* __restrict__ rp, DevFeatures* feat, long long n_cols,
-         long long hw, int* out_kernel, cudaGraphConditionalHandle cond, int use_cond) {
+         long long hw, int* out_kernel, cudaGraphConditionalHandle cond, int use_cond,
+         int* cache) {
     extern __shared__ double leaf[];  // [num_rounds * num_classes]
+    // The decision is a pure function of (matrix, model, N, hw): a graph that already
+    // made it re-applies it without walking the ensemble again.
+    if (cache != nullptr) {
+        const int cached = *cache;
+        if (cached >= 0) {
+            if (threadIdx.x == 0) {
+                *out_kernel = cached;
+                if (use_cond) cudaGraphSetConditional(cond, unsigned(cached));
+            }
+            return;
+        }
+    }
     __shared__ int ambiguous;
     __shared__ double s_exact;
     __shared__ int s_have;
@@ -346,6 +359,7 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
         for (int c = 1; c < num_classes; ++c)
             if (scores[c] > scores[best]) best = c;
         *out_kernel = best;
+        if (cache != nullptr) *cache = best;
         if (use_cond) cudaGraphSetConditional(cond, unsigned(best));
     }
 }
@@ -353,7 +367,8 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
 uint64_t model_generation(const daspmm_model* m) { return m->generation; }
 
 int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
-                  int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s) {
+                  int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s,
+                  int* cache) {
     const int ntrees = int(m->rounds.size()) * m->num_classes;
     const size_t smem = sizeof(double) * size_t(std::max(ntrees, 1));
     if (m->num_classes > kMaxClasses)
@@ -363,7 +378,7 @@ int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, in
         cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k_select<<<1, kSelThreads, smem, s>>>(m->d_nodes, m->d_tree_off, int(m->rounds.size()),
                                           m->num_classes, h->rp, h->d_feat, n_cols, hw, d_kernel,
-                                          cond, use_cond ? 1 : 0);
+                                          cond, use_cond ? 1 : 0, cache);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "select");
 }
@@ -416,7 +431,7 @@ int daspmm_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, in
     if (!m->d_nodes) return fail(DASPMM_ERR_CUDA, "select: model not resident on a device");
     DeviceGuard g(h->device);
     return launch_select(h, m, n_cols, hw, d_kernel, cudaGraphConditionalHandle{}, false,
-                         static_cast<cudaStream_t>(stream));
+                         static_cast<cudaStream_t>(stream), nullptr);
 }
 
 }  // extern "C"

@@ -288,3 +288,96 @@ def test_device_warp_primitives_bit_exact(sk, golden):
         assert list(out[starts]) == list(seg_sums[soff:soff + cnt])
         off += w
         soff += cnt
+
+
+def _golden_model(tag):
+    import os
+
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return open(os.path.join(gdir, f"selector_{tag}.txt")).read()
+
+
+def test_device_selector_bit_exact_with_host_predict(sk):
+    """daspmm_select (device features + device ensemble) == predict_kernel on
+    extract_features (host, reference arithmetic) for many matrices and N — with the
+    reference-trained golden model and with the shipped B200 model."""
+    import os
+
+    import torch
+
+    models = [sk.load_selector(_golden_model("plain")),
+              sk.load_selector(open(os.path.join(os.path.dirname(sk.__file__), "models",
+                                                 "b200_selector.txt")).read())]
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    n_checked = 0
+    for seed in range(12):
+        skew = [0.0, 0.8, 1.5][seed % 3]
+        rows = [300, 5000, 40000][seed % 3]
+        a = H.random_csr(rows, rows, rows * (2 + seed), seed=seed, dtype=np.float32, skew=skew)
+        d = sk.DeviceCsr.from_host(a)
+        for n in (1, 2, 3, 8, 16, 33, 64, 128, 1000):
+            f = sk.extract_features(d, n)
+            for m in models:
+                want = sk.predict_kernel(m, f).index()
+                sk.select_device(d, m, n, out)
+                torch.cuda.synchronize()
+                assert int(out.item()) == want, (seed, n)
+                n_checked += 1
+    assert n_checked >= 200
+
+
+def test_graph_dispatch_runs_the_selected_kernel(sk):
+    """spmm_selected: the SWITCH body that runs is the selector's choice, and the
+    output equals spmm with that kernel; both B layouts; repeated calls reuse the graph."""
+    import os
+
+    import torch
+
+    model = sk.load_selector(open(os.path.join(os.path.dirname(sk.__file__), "models",
+                                               "b200_selector.txt")).read())
+    for seed, skew in ((1, 0.0), (2, 1.5)):
+        a = H.random_csr(6000, 5000, 90000, seed=seed, dtype=np.float32, skew=skew)
+        d = sk.DeviceCsr.from_host(a)
+        y64 = None
+        for n in (2, 8, 32, 128):
+            x = np.random.default_rng(n).uniform(-1, 1, (5000, n)).astype(np.float32)
+            y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+            bound = H.gamma_bound(a, x, np.float32)
+            for layout in (sk.Layout.RowMajor, sk.Layout.ColMajor):
+                B = torch.from_numpy(np.ascontiguousarray(x if layout == sk.Layout.RowMajor
+                                                          else x.T)).cuda()
+                kout = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+                for rep in range(3):
+                    Cc = torch.full((6000, n), float("nan"), device="cuda")
+                    sk.spmm_selected(d, model, B, Cc, b_layout=layout, kernel_out=kout)
+                    torch.cuda.synchronize()
+                    y = Cc.cpu().numpy().astype(np.float64)
+                    assert (np.abs(y - y64) <= bound).all(), (n, layout, rep)
+                want = sk.predict_kernel(model, sk.extract_features(d, n)).index()
+                assert int(kout.item()) == want
+
+
+def test_row_panels_reassemble_exactly(sk):
+    """Multi-GPU unit on one device: nnz-balanced row panels (multi.row_panel_cuts)
+    computed separately and stacked equal the single-handle result bit for bit (RB
+    exact mode), i.e. sharding needs no exchange."""
+    import torch
+
+    from paper_2202_08556_b200 import multi
+
+    a = H.random_csr(5000, 4000, 120000, seed=8, dtype=np.float32, skew=1.3)
+    d = sk.DeviceCsr.from_host(a)
+    x = np.random.default_rng(3).uniform(-1, 1, (4000, 32)).astype(np.float32)
+    B = torch.from_numpy(x).cuda()
+    full = torch.empty(5000, 32, device="cuda")
+    sk.spmm_device(0, d, B, full, exact=True)
+    for parts in (2, 3, 8):
+        cuts = multi.row_panel_cuts(a.row_offsets, parts)
+        pieces = []
+        for p in range(parts):
+            pd = d.panel(int(cuts[p]), int(cuts[p + 1]))
+            Cp = torch.empty(int(cuts[p + 1] - cuts[p]), 32, device="cuda")
+            sk.spmm_device(0, pd, B, Cp, exact=True)
+            pieces.append(Cp)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(torch.cat(pieces).cpu().numpy(), full.cpu().numpy())
