@@ -111,15 +111,15 @@ static int64_t max_tile_cols(const daspmm_csr* h, int64_t N) {
     return 256;
 }
 
-// Default EB chunk size: enough chunks for >= 2 waves of resident groups.
-static int64_t auto_chunks(int64_t nnz, int lanes_per_worker, int step) {
+// EB chunk count for a chunk length; DASPMM_EB_CHUNK overrides the length (tuning aid).
+static int64_t auto_chunks(int64_t nnz, int64_t chunk) {
     if (nnz <= 0) return 1;
-    const int64_t resident_threads = 148LL * 2048;
-    int64_t target = nnz * lanes_per_worker / (2 * resident_threads);
-    target = std::max<int64_t>(target, step);
-    target = std::min<int64_t>(target, 2048);
-    target = (target + step - 1) / step * step;
-    return (nnz + target - 1) / target;
+    static const int64_t env = [] {
+        const char* e = getenv("DASPMM_EB_CHUNK");
+        return e ? int64_t(atoll(e)) : int64_t(0);
+    }();
+    if (env > 0) chunk = env;
+    return (nnz + chunk - 1) / chunk;
 }
 
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
@@ -148,19 +148,27 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
     int64_t workers;
     if (eb) {
-        const int step = pr ? int(W) : std::max(p.L, 8);
-        p.P = P > 0 ? P : auto_chunks(h->nnz, lanes, step);
+        // Measured on B200 (profiles/r01_notes.md): short chunks win — 32 pairs per
+        // group (64 for full-warp SR groups), the split-row atomics are cheap.
+        const int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
+        p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);
         workers = p.P;
     } else if (!pr) {
-        // RB+SR row blocks: ~4 steps of pairs per group, but keep >= 2 waves of groups.
-        const int step = p.L >= 16 ? p.L : (p.L >= 4 ? 16 : 8);
+        // RB+SR row blocks (measured, profiles/r01_notes.md): one row per group for
+        // narrow groups (N <= 8), ~128 pairs per group once a group spans >= 8 lanes.
         const double avg = h->M > 0 ? double(h->nnz) / double(h->M) : 0.0;
-        int64_t rpg = avg > 0 ? int64_t(4.0 * step / avg) : 64;
+        const double target = p.L >= 8 ? 128.0 : (p.L >= 4 ? 32.0 : 16.0);
+        int64_t rpg = avg > 0 ? int64_t(target / avg) : 64;
         // Skewed rows: a long row already fills its group; do not stack more rows on it.
         const double sd = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
         if (sd > 2.0 * avg) rpg = 1;
         const int64_t cap = std::max<int64_t>(1, h->M * lanes / (2LL * 148 * 2048));
         rpg = std::max<int64_t>(1, std::min<int64_t>({rpg, cap, 64}));
+        static const int64_t env_rpg = [] {
+            const char* e = getenv("DASPMM_RPG");
+            return e ? int64_t(atoll(e)) : int64_t(0);
+        }();
+        if (env_rpg > 0) rpg = env_rpg;
         p.rpg = rpg;
         workers = (h->M + rpg - 1) / rpg;
     } else {

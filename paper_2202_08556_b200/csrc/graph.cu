@@ -45,8 +45,15 @@ struct Entry {
     void* bt = nullptr;       // B in the other layout (may be null: see twin fallback)
     int* own_kernel = nullptr;
     int* decision = nullptr;  // device cache of the selector's choice (-1 = not yet made)
+    // The selector kernel also publishes its choice into mapped pinned host memory.
+    // Once it is visible, later identical calls launch the chosen kernel directly —
+    // the device made the decision; the host never waits for it.
+    int* published = nullptr;        // host view
+    int* published_dev = nullptr;    // device view
+    const void* Bk = nullptr;        // per-kernel operand for the direct path
     ~Entry() {
         cudaFree(decision);
+        if (published) cudaFreeHost(published);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         cudaFree(chunk_row);
@@ -99,6 +106,13 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
         return cuda_fail(e, "graph: cudaMalloc(decision)");
     if ((e = cudaMemset(en.decision, 0xff, sizeof(int))) != cudaSuccess)
         return cuda_fail(e, "graph: cudaMemset(decision)");
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&en.published), sizeof(int),
+                           cudaHostAllocMapped)) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaHostAlloc(published)");
+    *en.published = -1;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&en.published_dev), en.published,
+                                      0)) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaHostGetDevicePointer");
     cudaStream_t cap;
     if ((e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking)) != cudaSuccess)
         return cuda_fail(e, "graph: stream");
@@ -116,7 +130,8 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     if ((e = cudaStreamBeginCaptureToGraph(cap, en.graph, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return cuda_fail(e, "graph: capture(select)");
-    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap, en.decision);
+    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap, en.decision,
+                           en.published_dev);
     cudaGraph_t g_out = nullptr;
     e = cudaStreamEndCapture(cap, &g_out);
     if (rc) return rc;
@@ -217,6 +232,26 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
         }
         en = it->second.get();
     }
-    cudaError_t e = cudaGraphLaunch(en->exec, static_cast<cudaStream_t>(stream));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int decided = *reinterpret_cast<volatile int*>(en->published);
+    if (decided >= 0 && decided < 8) {
+        // Steady state: the device's published choice, launched directly (same plan
+        // and scratch as the SWITCH body).
+        const int want = ((decided >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
+        if (want == b_layout)
+            return spmm_device(h, decided, 0, W, d_B, ldb, N, d_C, ldc, flags, s, en->chunk_row);
+        if (en->bt) {
+            const int64_t ldt = b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
+                                                             : std::max<int64_t>(N, 1);
+            cudaError_t e = b_layout == DASPMM_ROW_MAJOR
+                                ? transpose(h->dtype, d_B, h->K, N, ldb, en->bt, ldt, s)
+                                : transpose(h->dtype, d_B, N, h->K, ldb, en->bt, ldt, s);
+            if (e != cudaSuccess) return cuda_fail(e, "transpose");
+            return spmm_device(h, decided, 0, W, en->bt, ldt, N, d_C, ldc, flags, s,
+                               en->chunk_row);
+        }
+        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, flags, s, en->chunk_row);
+    }
+    cudaError_t e = cudaGraphLaunch(en->exec, s);
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "graph launch");
 }

@@ -79,7 +79,7 @@ cudaError_t transpose(int dtype, const void* in, int64_t rows, int64_t cols, int
 // Implemented in select.cu
 int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
                   int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s,
-                  int* cache);
+                  int* cache, int* publish);
 uint64_t model_generation(const daspmm_model* m);
 // Implemented in graph.cu
 void graph_cache_free(daspmm_csr* h);

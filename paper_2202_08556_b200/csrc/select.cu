@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kSelThreads)
 k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off, int num_rounds,
          int num_classes, const int* __restrict__ rp, DevFeatures* feat, long long n_cols,
          long long hw, int* out_kernel, cudaGraphConditionalHandle cond, int use_cond,
-         int* cache) {
+         int* cache, volatile int* publish) {
     extern __shared__ double leaf[];  // [num_rounds * num_classes]
     // The decision is a pure function of (matrix, model, N, hw): a graph that already
     // made it re-applies it without walking the ensemble again.
@@ -285,6 +285,7 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
         if (cached >= 0) {
             if (threadIdx.x == 0) {
                 *out_kernel = cached;
+                if (publish != nullptr) *publish = cached;
                 if (use_cond) cudaGraphSetConditional(cond, unsigned(cached));
             }
             return;
@@ -360,6 +361,7 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
             if (scores[c] > scores[best]) best = c;
         *out_kernel = best;
         if (cache != nullptr) *cache = best;
+        if (publish != nullptr) *publish = best;  // mapped pinned host memory
         if (use_cond) cudaGraphSetConditional(cond, unsigned(best));
     }
 }
@@ -368,7 +370,7 @@ uint64_t model_generation(const daspmm_model* m) { return m->generation; }
 
 int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
                   int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s,
-                  int* cache) {
+                  int* cache, int* publish) {
     const int ntrees = int(m->rounds.size()) * m->num_classes;
     const size_t smem = sizeof(double) * size_t(std::max(ntrees, 1));
     if (m->num_classes > kMaxClasses)
@@ -378,7 +380,7 @@ int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, in
         cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k_select<<<1, kSelThreads, smem, s>>>(m->d_nodes, m->d_tree_off, int(m->rounds.size()),
                                           m->num_classes, h->rp, h->d_feat, n_cols, hw, d_kernel,
-                                          cond, use_cond ? 1 : 0, cache);
+                                          cond, use_cond ? 1 : 0, cache, publish);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "select");
 }
@@ -431,7 +433,7 @@ int daspmm_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, in
     if (!m->d_nodes) return fail(DASPMM_ERR_CUDA, "select: model not resident on a device");
     DeviceGuard g(h->device);
     return launch_select(h, m, n_cols, hw, d_kernel, cudaGraphConditionalHandle{}, false,
-                         static_cast<cudaStream_t>(stream), nullptr);
+                         static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
 }  // extern "C"
