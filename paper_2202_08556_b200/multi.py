@@ -60,7 +60,8 @@ def choose_partition(M: int, K: int, nnz: int, N: int, parts: int, elem: int = 4
 
 def gather_rows(local_c, cuts, group=None):
     """All-gather row panels of C (unequal sizes) into the full M x N matrix on every
-    rank: pad to the largest panel, one NCCL all-gather, then trim."""
+    rank: pad to the largest panel, one all-gather (NCCL over NVLink on GPUs, gloo on
+    CPU), then trim."""
     import torch
     import torch.distributed as dist
 
@@ -70,9 +71,9 @@ def gather_rows(local_c, cuts, group=None):
     n = local_c.shape[1]
     pad = torch.zeros(mx, n, dtype=local_c.dtype, device=local_c.device)
     pad[: local_c.shape[0]].copy_(local_c)
-    out = torch.empty(world * mx, n, dtype=local_c.dtype, device=local_c.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
-    return torch.cat([out[p * mx: p * mx + sizes[p]] for p in range(world)], 0)
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return torch.cat([outs[p][: sizes[p]] for p in range(world)], 0)
 
 
 def gather_cols(local_c, bounds, group=None):
@@ -86,6 +87,6 @@ def gather_cols(local_c, bounds, group=None):
     M = local_c.shape[0]
     pad = torch.zeros(M, mx, dtype=local_c.dtype, device=local_c.device)
     pad[:, : local_c.shape[1]].copy_(local_c)
-    out = torch.empty(world, M, mx, dtype=local_c.dtype, device=local_c.device)
-    dist.all_gather_into_tensor(out.view(world * M, mx), pad, group=group)
-    return torch.cat([out[p, :, : widths[p]] for p in range(world)], 1)
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return torch.cat([outs[p][:, : widths[p]] for p in range(world)], 1)
