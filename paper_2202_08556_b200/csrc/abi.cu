@@ -153,6 +153,13 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         const int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
         p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);
         workers = p.P;
+        if (!pr && !exact && P <= 0) {  // fast path: CTA-combined boundary rows
+            p.cta = true;
+            p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
+            p.sub = std::max<int64_t>(p.sub, 1);
+            p.P = (h->nnz + p.sub - 1) / p.sub;
+            workers = p.P;
+        }
     } else if (!pr) {
         // RB+SR row blocks (measured, profiles/r01_notes.md): one row per group for
         // narrow groups (N <= 8), ~128 pairs per group once a group spans >= 8 lanes.
@@ -200,11 +207,16 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     a.seg = int(std::max<int64_t>(W, 256));
     a.chunk_row = chunk_row;
     a.rpg = p.rpg;
+    a.sub = p.sub;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if (eb) {
-        cudaError_t e = launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,
-                                          static_cast<T*>(C), ldc, int(N), h->empty_rows,
-                                          int(h->n_empty), s);
+        cudaError_t e =
+            p.cta ? launch_eb_prep_uniform<T>(h->rp, int(h->M), h->nnz, p.sub, p.P, kThreads / p.L,
+                                              chunk_row, static_cast<T*>(C), ldc, int(N),
+                                              h->empty_rows, int(h->n_empty), s)
+                  : launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,
+                                      static_cast<T*>(C), ldc, int(N), h->empty_rows,
+                                      int(h->n_empty), s);
         if (e != cudaSuccess) return e;
         return pr ? launch_eb_pr<T>(p, a, s) : launch_eb_sr<T>(p, a, s);
     }

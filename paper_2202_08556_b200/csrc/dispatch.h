@@ -20,6 +20,8 @@ struct Plan {
     dim3 grid;
     int64_t P = 0;       // EB chunks
     int64_t rpg = 1;     // RB+SR rows per group (row-block size)
+    bool cta = false;    // EB+SR fast path: CTA-combined boundary rows (k_eb_sr_cta)
+    int64_t sub = 0;     // ... its pairs per group sub-chunk
 };
 
 // Each returns cudaErrorNotSupported for a shape with no instantiation.
@@ -27,6 +29,10 @@ template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, 
 template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+template <typename T>
+cudaError_t launch_eb_prep_uniform(const int* rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
+                                   int G, int* chunk_row, T* C, int64_t ldc, int N,
+                                   const int* empty_rows, int n_empty, cudaStream_t s);
 template <typename T>
 cudaError_t launch_eb_prep(const int* rp, int M, int64_t nnz, int64_t P, int* chunk_row, T* C,
                            int64_t ldc, int N, const int* empty_rows, int n_empty, cudaStream_t s);

@@ -38,6 +38,7 @@ struct SpmmArgs {
     int64_t P;                   // EB workers (chunks)
     int seg;                     // exact-mode EB+SR staging segment, max(W, 256)
     int64_t rpg;                 // RB: rows per group (row-block size)
+    int64_t sub;                 // EB fast path: pairs per group sub-chunk
     const int* __restrict__ chunk_row;  // EB: row holding each chunk's first element
 };
 
@@ -64,10 +65,26 @@ __device__ __forceinline__ Frag<T, V> gather(const SpmmArgs<T>& a, int k, int co
 //               Exact mode restarts the run at the reference's staging boundaries
 //               (seg_cap = max(W, 256), spmm.hpp:50, 136) and adds the partials in
 //               the reference's order.
-template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, bool EB>
+// Boundary partials of one CTA (EB fast path): slot b holds the pieces of the row
+// that crosses sub-chunk boundary b — L[b] from the group before it, R[b] from the
+// group after it.
+template <typename T>
+struct CtaSlots {
+    T* L;      // [(G+1) * TN]
+    T* R;      // [(G+1) * TN]
+    int* row;  // [G+1], -1 when no row crosses the boundary
+    int g;     // this group's index in the CTA
+    int tile0; // first column of the CTA's column tile
+    int tn;    // tile width
+};
+
+enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2 };
+
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE>
 __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, const int e1, int r,
                                         const int r_end, const int n0, const unsigned mask,
-                                        const int gl) {
+                                        const int gl, const CtaSlots<T>* slots = nullptr) {
+    constexpr bool EB = MODE != kRB;
     constexpr int STEP = LPR >= 16 ? LPR : (LPR >= 4 ? 16 : 8);  // pairs per group per step
     constexpr int EPL = STEP / LPR;                              // pairs per lane per step
     // Double-buffered A pairs pay off once a lane holds few of them (LPR >= 4); narrow
@@ -97,6 +114,17 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                 acc[s].v[i] = ydep[s].v[i] = T(0);
             }
             const int col = n0 + s * LPR * V;
+            if constexpr (MODE == kEBCta) {
+                if (!owned) {  // boundary piece -> shared slot, combined by the CTA
+                    const int b = rstart < e0 ? slots->g : slots->g + 1;
+                    T* dst = (rstart < e0 ? slots->R : slots->L) + b * slots->tn +
+                             (col - slots->tile0);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) dst[i] = out.v[i];
+                    if (s == 0 && gl == 0) slots->row[b] = r;
+                    continue;
+                }
+            }
             if (col < a.N) {
                 T* y = a.C + int64_t(r) * a.ldc + col;
                 if (owned) st_frag(y, out);
@@ -224,8 +252,8 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     if (r0 >= a.M) return;  // whole group leaves together
     const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
     const int n0 = blockIdx.y * TN + gl * V;
-    sr_walk<T, CM, EXACT, V, LPR, CPL, false>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0), r1,
-                                              n0, mask, gl);
+    sr_walk<T, CM, EXACT, V, LPR, CPL, kRB>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0), r1,
+                                            n0, mask, gl);
 }
 
 // EB + SR: group w owns partition chunk w (partition.hpp:45-64).
@@ -240,8 +268,91 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     chunk_bounds(a.nnz, a.P, w, e0, e1);
     if (e0 >= e1) return;
     const int n0 = blockIdx.y * TN + gl * V;
-    sr_walk<T, CM, EXACT, V, LPR, CPL, true>(a, int(e0), int(e1), a.chunk_row[w], a.M, n0, mask,
-                                             gl);
+    sr_walk<T, CM, EXACT, V, LPR, CPL, kEB>(a, int(e0), int(e1), a.chunk_row[w], a.M, n0, mask,
+                                            gl);
+}
+
+// EB + SR, fast path: a CTA owns G = 256/LPR consecutive sub-chunks of a.sub pairs,
+// one per lane group. Rows crossing a sub-chunk boundary inside the CTA are summed in
+// shared memory and stored once; only rows crossing the CTA's own range take an
+// atomic (pre-zeroed by k_eb_prep_uniform). Long power-law rows thus receive one
+// atomic per CTA instead of one per group.
+template <typename T, bool CM, int V, int LPR, int CPL>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4)
+k_eb_sr_cta(const SpmmArgs<T> a) {
+    constexpr int G = kThreads / LPR;
+    constexpr int TN = LPR * V * CPL;
+    __shared__ T sL[(G + 1) * TN];
+    __shared__ T sR[(G + 1) * TN];
+    __shared__ int srow[G + 1];
+    for (int i = threadIdx.x; i < (G + 1) * TN; i += kThreads) sL[i] = sR[i] = T(0);
+    for (int i = threadIdx.x; i < G + 1; i += kThreads) srow[i] = -1;
+    __syncthreads();
+
+    const unsigned mask = group_mask<LPR>();
+    const int gl = threadIdx.x & (LPR - 1);
+    const int g = threadIdx.x / LPR;
+    const int64_t E0 = int64_t(blockIdx.x) * G * a.sub;
+    const int64_t E1 = min(a.nnz, E0 + int64_t(G) * a.sub);
+    const int64_t e0 = E0 + int64_t(g) * a.sub;
+    const int64_t e1 = min(E1, e0 + a.sub);
+    const int tile0 = blockIdx.y * TN;
+    const int n0 = tile0 + gl * V;
+    CtaSlots<T> slots{sL, sR, srow, g, tile0, TN};
+    if (e0 < e1)
+        sr_walk<T, CM, false, V, LPR, CPL, kEBCta>(a, int(e0), int(e1),
+                                                   a.chunk_row[int64_t(blockIdx.x) * G + g], a.M,
+                                                   n0, mask, gl, &slots);
+    __syncthreads();
+    // Combine: thread t owns tile column t; boundaries in order, segmented by row.
+    for (int t = threadIdx.x; t < TN; t += kThreads) {
+        const int col = tile0 + t;
+        if (col >= a.N) continue;
+        int cur = -1;
+        T acc = T(0);
+        auto deposit = [&](int row, T v) {
+            T* y = a.C + int64_t(row) * a.ldc + col;
+            if (__ldg(a.rp + row) >= E0 && __ldg(a.rp + row + 1) <= E1) *y = v;
+            else atomicAdd(y, v);
+        };
+        for (int b = 0; b <= G; ++b) {
+            const int row = srow[b];
+            if (row < 0) continue;
+            const T v = sL[b * TN + t] + sR[b * TN + t];
+            if (row != cur) {
+                if (cur >= 0) deposit(cur, acc);
+                cur = row;
+                acc = v;
+            } else {
+                acc += v;
+            }
+        }
+        if (cur >= 0) deposit(cur, acc);
+    }
+}
+
+// Prologue of the EB fast path: uniform sub-chunks of `sub` pairs; chunk_row for every
+// sub-chunk (row of its first pair, by binary search), split-row zeroing only at CTA
+// boundaries (every G-th sub-chunk), empty rows from the handle's list.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+k_eb_prep_uniform(const int* __restrict__ rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
+                  int G, int* __restrict__ chunk_row, T* C, int64_t ldc, int N,
+                  const int* __restrict__ empty_rows, int n_empty) {
+    const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (tid < n_sub) {
+        const int64_t b = tid * sub;
+        const int row = b < nnz ? row_of_element(rp, M, int(b)) : M;
+        chunk_row[tid] = row;
+        if (tid % G == 0 && b < nnz && __ldg(rp + row) < b) {
+            T* y = C + int64_t(row) * ldc;
+            for (int n = 0; n < N; ++n) y[n] = T(0);
+        }
+    } else if (tid - n_sub < int64_t(n_empty) * N) {
+        const int64_t k = tid - n_sub;
+        const int r = empty_rows[k / N];
+        C[int64_t(r) * ldc + k % N] = T(0);
+    }
 }
 
 // =============================================================== RB + PR (K1 / K3)

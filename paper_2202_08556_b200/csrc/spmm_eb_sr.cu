@@ -1,7 +1,72 @@
 // EB+SR launchers (K4 EB+RM+SR, K6 EB+CM+SR) and the EB partition/zeroing prologue.
 #include "launch_sr.cuh"
 namespace daspmm {
+// Fast path instantiations (CTA-combined boundary rows); the exact path keeps one
+// partition chunk per group (k_eb_sr) so owned rows match the reference bit for bit.
+#define DASPMM_CTA_LPR_TABLE(T, CM, V)                                                      \
+    switch (p.L) {                                                                        \
+        case 1: k_eb_sr_cta<T, CM, V, 1, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
+        case 2: k_eb_sr_cta<T, CM, V, 2, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
+        case 4: k_eb_sr_cta<T, CM, V, 4, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
+        case 8: k_eb_sr_cta<T, CM, V, 8, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
+        case 16: k_eb_sr_cta<T, CM, V, 16, 1><<<p.grid, kThreads, 0, s>>>(a); break;      \
+        case 32:                                                                          \
+            if (p.X == 2) k_eb_sr_cta<T, CM, V, 32, 2><<<p.grid, kThreads, 0, s>>>(a);    \
+            else k_eb_sr_cta<T, CM, V, 32, 1><<<p.grid, kThreads, 0, s>>>(a);             \
+            break;                                                                        \
+        default: return cudaErrorNotSupported;                                            \
+    }
+
+template <typename T>
+static cudaError_t launch_eb_sr_cta(const Plan& p, const SpmmArgs<T>& a, cudaStream_t s) {
+    if (p.cm) {
+        if (p.V != 1) return cudaErrorNotSupported;
+        DASPMM_CTA_LPR_TABLE(T, true, 1)
+    } else if (p.V == 1) {
+        DASPMM_CTA_LPR_TABLE(T, false, 1)
+    } else if (p.V == 2) {
+        DASPMM_CTA_LPR_TABLE(T, false, 2)
+    } else if constexpr (sizeof(T) == 4) {
+        if (p.V == 4) { DASPMM_CTA_LPR_TABLE(T, false, 4) }
+        else return cudaErrorNotSupported;
+    } else {
+        return cudaErrorNotSupported;
+    }
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_eb_sr_per_chunk(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+#define launch_eb_sr launch_eb_sr_per_chunk
 DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
+#undef launch_eb_sr
+
+template <>
+cudaError_t launch_eb_sr<float>(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    return p.cta ? launch_eb_sr_cta<float>(p, a, s) : launch_eb_sr_per_chunk<float>(p, a, s);
+}
+template <>
+cudaError_t launch_eb_sr<double>(const Plan& p, const SpmmArgs<double>& a, cudaStream_t s) {
+    return p.cta ? launch_eb_sr_cta<double>(p, a, s) : launch_eb_sr_per_chunk<double>(p, a, s);
+}
+
+template <typename T>
+cudaError_t launch_eb_prep_uniform(const int* rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
+                                   int G, int* chunk_row, T* C, int64_t ldc, int N,
+                                   const int* empty_rows, int n_empty, cudaStream_t s) {
+    const int64_t work = n_sub + int64_t(n_empty) * N;
+    if (work == 0) return cudaSuccess;
+    const int64_t blocks = (work + kThreads - 1) / kThreads;
+    k_eb_prep_uniform<T><<<dim3(unsigned(blocks)), kThreads, 0, s>>>(
+        rp, M, nnz, sub, n_sub, G, chunk_row, C, ldc, N, empty_rows, n_empty);
+    return cudaGetLastError();
+}
+template cudaError_t launch_eb_prep_uniform<float>(const int*, int, int64_t, int64_t, int64_t, int,
+                                                   int*, float*, int64_t, int, const int*, int,
+                                                   cudaStream_t);
+template cudaError_t launch_eb_prep_uniform<double>(const int*, int, int64_t, int64_t, int64_t,
+                                                    int, int*, double*, int64_t, int, const int*,
+                                                    int, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_eb_prep(const int* rp, int M, int64_t nnz, int64_t P, int* chunk_row, T* C,
