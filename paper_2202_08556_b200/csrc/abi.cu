@@ -170,12 +170,12 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         const double sd = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
         if (sd > 2.0 * avg) rpg = 1;
         const int64_t cap = std::max<int64_t>(1, h->M * lanes / (2LL * 148 * 2048));
-        rpg = std::max<int64_t>(1, std::min<int64_t>({rpg, cap, 64}));
+        rpg = std::max<int64_t>(1, std::min<int64_t>({rpg, cap, int64_t(p.L)}));  // <= LPR
         static const int64_t env_rpg = [] {
             const char* e = getenv("DASPMM_RPG");
             return e ? int64_t(atoll(e)) : int64_t(0);
         }();
-        if (env_rpg > 0) rpg = env_rpg;
+        if (env_rpg > 0) rpg = std::min<int64_t>(env_rpg, p.L);
         p.rpg = rpg;
         workers = (h->M + rpg - 1) / rpg;
     } else {
@@ -208,15 +208,16 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     a.chunk_row = chunk_row;
     a.rpg = p.rpg;
     a.sub = p.sub;
+    a.rows = h->coo_rows;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if (eb) {
         cudaError_t e =
-            p.cta ? launch_eb_prep_uniform<T>(h->rp, int(h->M), h->nnz, p.sub, p.P, kThreads / p.L,
-                                              chunk_row, static_cast<T*>(C), ldc, int(N),
-                                              h->empty_rows, int(h->n_empty), s)
+            p.cta ? launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, kThreads / p.L,
+                                              static_cast<T*>(C), ldc, int(N), h->empty_rows,
+                                              int(h->n_empty), s)
                   : launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,
                                       static_cast<T*>(C), ldc, int(N), h->empty_rows,
-                                      int(h->n_empty), s);
+                                      int(h->n_empty), h->coo_rows, s);
         if (e != cudaSuccess) return e;
         return pr ? launch_eb_pr<T>(p, a, s) : launch_eb_sr<T>(p, a, s);
     }
@@ -236,7 +237,8 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     int* chunk_row = chunk_scratch;
     const bool own_scratch = chunk_scratch == nullptr;
     cudaError_t e;
-    if (kernel >= 4 && own_scratch) {
+    if (kernel >= 4 && own_scratch) {  // (graph bodies get the COO array built beforehand)
+        if (int rc = ensure_coo(h, s)) return rc;
         if ((e = cudaMallocAsync(&chunk_row, sizeof(int) * size_t(std::max<int64_t>(p.P, 1)), s)) !=
             cudaSuccess)
             return cuda_fail(e, "cudaMallocAsync(chunk_row)");
@@ -502,6 +504,7 @@ int daspmm_csr_destroy(daspmm_csr* h) {
     }
     cudaFree(h->empty_rows);
     cudaFree(h->d_feat);
+    cudaFree(h->coo_rows);
     delete h;
     return DASPMM_OK;
 }
@@ -622,7 +625,8 @@ int daspmm_partition(const daspmm_csr* h, int64_t p, int64_t* begin, int64_t* en
     cudaError_t e = cudaMalloc(&d_row, sizeof(int) * size_t(p));
     if (e != cudaSuccess) return cuda_fail(e, "partition: cudaMalloc");
     // The EB prologue kernel with no output rows to zero (C = null, N = 0).
-    e = launch_eb_prep<float>(h->rp, int(h->M), h->nnz, p, d_row, nullptr, 0, 0, nullptr, 0, 0);
+    e = launch_eb_prep<float>(h->rp, int(h->M), h->nnz, p, d_row, nullptr, 0, 0, nullptr, 0,
+                              nullptr, 0);
     std::vector<int> rows(size_t(p), 0);
     if (e == cudaSuccess)
         e = cudaMemcpy(rows.data(), d_row, sizeof(int) * size_t(p), cudaMemcpyDeviceToHost);

@@ -30,11 +30,13 @@ template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, 
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T>
-cudaError_t launch_eb_prep_uniform(const int* rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
-                                   int G, int* chunk_row, T* C, int64_t ldc, int N,
-                                   const int* empty_rows, int n_empty, cudaStream_t s);
+cudaError_t launch_eb_prep_uniform(const int* rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
+                                   T* C, int64_t ldc, int N, const int* empty_rows, int n_empty,
+                                   cudaStream_t s);
+// rows == nullptr: partition_elements API (writes chunk_row); else SpMM zeroing only.
 template <typename T>
 cudaError_t launch_eb_prep(const int* rp, int M, int64_t nnz, int64_t P, int* chunk_row, T* C,
-                           int64_t ldc, int N, const int* empty_rows, int n_empty, cudaStream_t s);
+                           int64_t ldc, int N, const int* empty_rows, int n_empty,
+                           const int* rows, cudaStream_t s);
 
 }  // namespace daspmm

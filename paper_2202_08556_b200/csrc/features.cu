@@ -76,6 +76,28 @@ __global__ void k_std_sequential(const int* __restrict__ rp, int M, DevFeatures*
     f->exact_valid = 1;
 }
 
+// One warp per row writes the row's id into its nonzeros' slots (COO expansion).
+__global__ void k_coo_rows(const int* __restrict__ rp, int M, int* __restrict__ rows) {
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= M) return;
+    const int r = int(warp);
+    const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+    for (int i = s + lane; i < e; i += 32) rows[i] = r;
+}
+
+int ensure_coo(const daspmm_csr* hc, cudaStream_t s) {
+    daspmm_csr* h = const_cast<daspmm_csr*>(hc);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->coo_rows || h->nnz == 0) return DASPMM_OK;
+    cudaError_t e = cudaMalloc(&h->coo_rows, sizeof(int32_t) * size_t(h->nnz));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(coo_rows)");
+    const int64_t threads = h->M * 32;
+    k_coo_rows<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, int(h->M), h->coo_rows);
+    e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "coo_rows");
+}
+
 int compute_features(daspmm_csr* h, cudaStream_t s) {
     const int M = int(h->M);
     DevFeatures f{};

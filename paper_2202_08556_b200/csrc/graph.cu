@@ -84,6 +84,7 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
             return cuda_fail(e, "graph: cudaMalloc");
         d_kernel = en.own_kernel;
     }
+    if (int rc = ensure_coo(h, 0)) return rc;  // EB bodies read COO row ids
     // Scratch: EB chunk rows for the largest plan, and B in the other layout.
     int64_t max_p = 1;
     for (int kid = 4; kid < 8; ++kid) {

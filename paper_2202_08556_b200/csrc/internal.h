@@ -59,11 +59,14 @@ struct daspmm_csr {
     daspmm::DevFeatures h_feat{};           // host mirror (filled at creation)
     std::mutex mu;                          // guards the lazy exact-std cache
     void* graph_cache = nullptr;            // graph.cu
+    int32_t* coo_rows = nullptr;            // EB kernels: row id per nonzero (built lazily)
 };
 
 namespace daspmm {
 // Implemented in features.cu
 int compute_features(daspmm_csr* h, cudaStream_t s);
+// Builds h->coo_rows once (never call inside a stream capture).
+int ensure_coo(const daspmm_csr* h, cudaStream_t s);
 int exact_std(daspmm_csr* h, double* out);
 // Implemented in abi.cu
 struct Plan;

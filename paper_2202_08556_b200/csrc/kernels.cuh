@@ -40,6 +40,7 @@ struct SpmmArgs {
     int64_t rpg;                 // RB: rows per group (row-block size)
     int64_t sub;                 // EB fast path: pairs per group sub-chunk
     const int* __restrict__ chunk_row;  // EB: row holding each chunk's first element
+    const int* __restrict__ rows;       // EB: COO row id of every nonzero (handle-owned)
 };
 
 constexpr int kThreads = 256;
@@ -82,7 +83,7 @@ enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2 };
 
 template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE>
 __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, const int e1, int r,
-                                        const int r_end, const int n0, const unsigned mask,
+                                        const int nrows, const int n0, const unsigned mask,
                                         const int gl, const CtaSlots<T>* slots = nullptr) {
     constexpr bool EB = MODE != kRB;
     constexpr int STEP = LPR >= 16 ? LPR : (LPR >= 4 ? 16 : 8);  // pairs per group per step
@@ -98,13 +99,31 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
     for (int s = 0; s < CPL; ++s)
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[s].v[i] = ydep[s].v[i] = T(0);
-    int rstart = __ldg(a.rp + r), rend = __ldg(a.rp + r + 1);
-    bool has = false;
     int next_seg = e0 + a.seg;
 
+    // Row bookkeeping without dependent loads.
+    //   RB: the block's nrows (<= LPR) row ends, one per lane, fetched once.
+    //   EB: per-pair row ids from the handle's COO array; a row is split only if it is
+    //       the range's first row and began before e0, or its last row and continues
+    //       past e1.
+    const int r0 = r;
+    int wend = 0, rend = 0;
+    int first_row = 0, last_row = 0;
+    bool first_split = false, last_split = false;
+    if constexpr (!EB) {
+        wend = gl < nrows ? __ldg(a.rp + r0 + 1 + gl) : INT_MAX;
+        rend = gshfl<LPR>(mask, wend, 0);
+    } else {
+        first_row = r;
+        last_row = __ldg(a.rows + e1 - 1);
+        first_split = e0 > 0 && __ldg(a.rows + e0 - 1) == first_row;
+        last_split = e1 < a.nnz && __ldg(a.rows + e1) == last_row;
+    }
+
     auto flush = [&]() {  // row r is complete within this range
-        if (EB && !has) return;
-        const bool owned = !EB || (rstart >= e0 && rend <= e1);
+        const bool head = EB && first_split && r == first_row;
+        const bool tail = EB && last_split && r == last_row;
+        const bool owned = !head && !tail;
 #pragma unroll
         for (int s = 0; s < CPL; ++s) {
             Frag<T, V> out;
@@ -116,9 +135,8 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
             const int col = n0 + s * LPR * V;
             if constexpr (MODE == kEBCta) {
                 if (!owned) {  // boundary piece -> shared slot, combined by the CTA
-                    const int b = rstart < e0 ? slots->g : slots->g + 1;
-                    T* dst = (rstart < e0 ? slots->R : slots->L) + b * slots->tn +
-                             (col - slots->tile0);
+                    const int b = head ? slots->g : slots->g + 1;
+                    T* dst = (head ? slots->R : slots->L) + b * slots->tn + (col - slots->tile0);
 #pragma unroll
                     for (int i = 0; i < V; ++i) dst[i] = out.v[i];
                     if (s == 0 && gl == 0) slots->row[b] = r;
@@ -131,49 +149,40 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                 else atomic_add_frag(y, out);
             }
         }
-        has = false;
     };
 
-    int c[EPL];
+    int c[EPL], rr[EB ? EPL : 1];
     T v[EPL];
-    if constexpr (PREFETCH) {
+    auto load_step = [&](int j, int* cc, T* vvv, int* rrr) {
 #pragma unroll
         for (int q = 0; q < EPL; ++q) {
-            const int e = e0 + q * LPR + gl;
-            c[q] = e < e1 ? ld_stream(a.ci + e) : 0;
-            v[q] = e < e1 ? ld_stream(a.va + e) : T(0);
+            const int e = j + q * LPR + gl;
+            const bool ok = e < e1;
+            cc[q] = ok ? ld_stream(a.ci + e) : 0;
+            vvv[q] = ok ? ld_stream(a.va + e) : T(0);
+            if constexpr (EB) rrr[q] = ok ? ld_stream(a.rows + e) : INT_MAX;
         }
-    }
+    };
+    if constexpr (PREFETCH) load_step(e0, c, v, rr);
     for (int j = e0; j < e1; j += STEP) {
-        int cn[PREFETCH ? EPL : 1];
+        int cn[PREFETCH ? EPL : 1], rn[(PREFETCH && EB) ? EPL : 1];
         T vn[PREFETCH ? EPL : 1];
-        if constexpr (PREFETCH) {
-#pragma unroll
-            for (int q = 0; q < EPL; ++q) {  // prefetch the next step
-                const int e = j + STEP + q * LPR + gl;
-                cn[q] = e < e1 ? ld_stream(a.ci + e) : 0;
-                vn[q] = e < e1 ? ld_stream(a.va + e) : T(0);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < EPL; ++q) {
-                const int e = j + q * LPR + gl;
-                c[q] = e < e1 ? ld_stream(a.ci + e) : 0;
-                v[q] = e < e1 ? ld_stream(a.va + e) : T(0);
-            }
-        }
+        if constexpr (PREFETCH) load_step(j + STEP, cn, vn, rn);  // next step in flight
+        else load_step(j, c, v, rr);
         const int cnt = min(STEP, e1 - j);
 #pragma unroll
         for (int x0 = 0; x0 < STEP; x0 += BATCH) {
             if (x0 < cnt) {  // group-uniform
                 const int nb = min(BATCH, cnt - x0);
                 T vv[BATCH];
+                int rid[EB ? BATCH : 1];
                 Frag<T, V> b[BATCH][CPL];
 #pragma unroll
                 for (int u = 0; u < BATCH; ++u) {
                     const int x = x0 + u;
                     const int ct = gshfl<LPR>(mask, c[x / LPR], x % LPR);
                     vv[u] = gshfl<LPR>(mask, v[x / LPR], x % LPR);
+                    if constexpr (EB) rid[u] = gshfl<LPR>(mask, rr[x / LPR], x % LPR);
                     // padded tail entries gather row 0 of B harmlessly and are never summed
 #pragma unroll
                     for (int s = 0; s < CPL; ++s) {
@@ -183,7 +192,10 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                 }
                 const int ef = j + x0;
                 const bool seg_in_batch = EB && EXACT && next_seg >= ef && next_seg < ef + nb;
-                if (nb == BATCH && ef + BATCH <= rend && !seg_in_batch) {
+                bool same_row;
+                if constexpr (EB) same_row = nb == BATCH && rid[BATCH - 1] == r;
+                else same_row = nb == BATCH && ef + BATCH <= rend;
+                if (same_row && !seg_in_batch) {
                     // fast path: the whole batch continues the current row
 #pragma unroll
                     for (int u = 0; u < BATCH; ++u)
@@ -192,17 +204,22 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 #pragma unroll
                             for (int i = 0; i < V; ++i)
                                 acc[s].v[i] = madd<EXACT>(acc[s].v[i], vv[u], b[u][s].v[i]);
-                    has = true;
                 } else {
 #pragma unroll
                     for (int u = 0; u < BATCH; ++u) {
                         if (u < nb) {
                             const int e = ef + u;
-                            while (e >= rend) {  // row change; steps over empty rows
-                                flush();
-                                ++r;
-                                rstart = rend;
-                                rend = __ldg(a.rp + r + 1);
+                            if constexpr (EB) {
+                                if (rid[u] != r) {  // row change (empty rows pre-zeroed)
+                                    flush();
+                                    r = rid[u];
+                                }
+                            } else {
+                                while (e >= rend) {  // row change; empty rows get zeros
+                                    flush();
+                                    ++r;
+                                    rend = gshfl<LPR>(mask, wend, r - r0);
+                                }
                             }
                             if constexpr (EB && EXACT) {
                                 if (e == next_seg) {  // reference staging boundary
@@ -216,7 +233,6 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                                     next_seg += a.seg;
                                 }
                             }
-                            has = true;
 #pragma unroll
                             for (int s = 0; s < CPL; ++s)
 #pragma unroll
@@ -232,16 +248,18 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
             for (int q = 0; q < EPL; ++q) {
                 c[q] = cn[q];
                 v[q] = vn[q];
+                if constexpr (EB) rr[q] = rn[q];
             }
         }
     }
+    if (EB && e0 >= e1) return;
     flush();
     if constexpr (!EB) {  // trailing empty rows of the block
-        for (++r; r < r_end; ++r) flush();
+        for (++r; r < r0 + nrows; ++r) flush();
     }
 }
 
-// RB + SR: group g owns rows [g*rpg, (g+1)*rpg) — a row block, balanced by row count.
+// RB + SR: group g owns rows [g*rpg, (g+1)*rpg) — a row block (rpg <= LPR).
 template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4) k_rb_sr(const SpmmArgs<T> a) {
     constexpr int TN = LPR * V * CPL;
@@ -252,8 +270,8 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     if (r0 >= a.M) return;  // whole group leaves together
     const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
     const int n0 = blockIdx.y * TN + gl * V;
-    sr_walk<T, CM, EXACT, V, LPR, CPL, kRB>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0), r1,
-                                            n0, mask, gl);
+    sr_walk<T, CM, EXACT, V, LPR, CPL, kRB>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0),
+                                            r1 - int(r0), n0, mask, gl);
 }
 
 // EB + SR: group w owns partition chunk w (partition.hpp:45-64).
@@ -268,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     chunk_bounds(a.nnz, a.P, w, e0, e1);
     if (e0 >= e1) return;
     const int n0 = blockIdx.y * TN + gl * V;
-    sr_walk<T, CM, EXACT, V, LPR, CPL, kEB>(a, int(e0), int(e1), a.chunk_row[w], a.M, n0, mask,
+    sr_walk<T, CM, EXACT, V, LPR, CPL, kEB>(a, int(e0), int(e1), __ldg(a.rows + e0), 0, n0, mask,
                                             gl);
 }
 
@@ -300,9 +318,8 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
     const int n0 = tile0 + gl * V;
     CtaSlots<T> slots{sL, sR, srow, g, tile0, TN};
     if (e0 < e1)
-        sr_walk<T, CM, false, V, LPR, CPL, kEBCta>(a, int(e0), int(e1),
-                                                   a.chunk_row[int64_t(blockIdx.x) * G + g], a.M,
-                                                   n0, mask, gl, &slots);
+        sr_walk<T, CM, false, V, LPR, CPL, kEBCta>(a, int(e0), int(e1), __ldg(a.rows + e0), 0, n0,
+                                                   mask, gl, &slots);
     __syncthreads();
     // Combine: thread t owns tile column t; boundaries in order, segmented by row.
     for (int t = threadIdx.x; t < TN; t += kThreads) {
@@ -336,17 +353,17 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
 // boundaries (every G-th sub-chunk), empty rows from the handle's list.
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-k_eb_prep_uniform(const int* __restrict__ rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
-                  int G, int* __restrict__ chunk_row, T* C, int64_t ldc, int N,
-                  const int* __restrict__ empty_rows, int n_empty) {
+k_eb_prep_uniform(const int* __restrict__ rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
+                  T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty) {
     const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (tid < n_sub) {
         const int64_t b = tid * sub;
-        const int row = b < nnz ? row_of_element(rp, M, int(b)) : M;
-        chunk_row[tid] = row;
-        if (tid % G == 0 && b < nnz && __ldg(rp + row) < b) {
-            T* y = C + int64_t(row) * ldc;
-            for (int n = 0; n < N; ++n) y[n] = T(0);
+        if (tid % G == 0 && b > 0 && b < nnz) {
+            const int row = __ldg(rows + b);
+            if (__ldg(rows + b - 1) == row) {
+                T* y = C + int64_t(row) * ldc;
+                for (int n = 0; n < N; ++n) y[n] = T(0);
+            }
         }
     } else if (tid - n_sub < int64_t(n_empty) * N) {
         const int64_t k = tid - n_sub;
@@ -424,16 +441,23 @@ __global__ void __launch_bounds__(kThreads) k_rb_pr(const SpmmArgs<T> a) {
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
 k_eb_prep(const int* __restrict__ rp, int M, int64_t nnz, int64_t P, int* __restrict__ chunk_row,
-          T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty) {
+          T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty,
+          const int* __restrict__ rows) {
     const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (tid < P) {
         int64_t b, e;
         chunk_bounds(nnz, P, tid, b, e);
-        const int row = b < nnz ? row_of_element(rp, M, int(b)) : M;
-        chunk_row[tid] = row;
-        if (b < nnz && __ldg(rp + row) < b) {
-            T* y = C + int64_t(row) * ldc;
-            for (int n = 0; n < N; ++n) y[n] = T(0);
+        if (rows != nullptr) {  // SpMM path: COO ids make the split test a compare
+            if (b > 0 && b < nnz) {
+                const int row = __ldg(rows + b);
+                if (__ldg(rows + b - 1) == row) {
+                    T* y = C + int64_t(row) * ldc;
+                    for (int n = 0; n < N; ++n) y[n] = T(0);
+                }
+            }
+        } else {  // partition_elements API: chunk-start rows by binary search
+            const int row = b < nnz ? row_of_element(rp, M, int(b)) : M;
+            chunk_row[tid] = row;
         }
     } else if (tid - P < int64_t(n_empty) * N) {
         const int64_t k = tid - P;
@@ -444,43 +468,11 @@ k_eb_prep(const int* __restrict__ rp, int M, int64_t nnz, int64_t P, int* __rest
 
 // =============================================================== EB + PR (K5 / K7)
 // W lanes take W consecutive nonzeros of the chunk (tiles at e0 + m*W, as the
-// reference's groups, spmm.hpp:164-183). Each lane resolves its element's row with
-// a shuffle binary search over W row offsets, the gated scan sums each row run,
-// and the run's first lane deposits: a row owned by the chunk is stored on its
+// reference's groups, spmm.hpp:164-183). Each lane reads its element's row id from
+// the handle's COO array, the gated scan sums each row run, and the run's first lane
+// deposits: a row owned by the chunk is stored on its
 // first tile and read-modify-written on later tiles (y += seg, the reference's
 // deposit order), a split row takes an atomic add.
-template <int W>
-__device__ __forceinline__ void resolve_rows(unsigned mask, const int* __restrict__ rp, int M,
-                                             int e, bool valid, int cur, int cur_start,
-                                             int& row, int& rs, int& re) {
-    int base = cur, base_start = cur_start;
-    bool done = !valid;
-    row = M;
-    rs = re = 0;
-    while (true) {
-        const int idx = base + 1 + (threadIdx.x & (W - 1));
-        const int b = idx <= M ? __ldg(rp + idx) : INT_MAX;
-        const int blast = __shfl_sync(mask, b, W - 1, W);
-        int cnt = 0;
-#pragma unroll
-        for (int s = W / 2; s >= 1; s >>= 1) {
-            const int bb = __shfl_sync(mask, b, cnt + s - 1, W);
-            if (bb <= e) cnt += s;
-        }
-        const int bprev = __shfl_sync(mask, b, cnt > 0 ? cnt - 1 : 0, W);
-        const int bcur = __shfl_sync(mask, b, cnt, W);
-        if (!done && e < blast) {
-            row = base + cnt;
-            rs = cnt > 0 ? bprev : base_start;
-            re = bcur;
-            done = true;
-        }
-        if (!__any_sync(mask, !done)) break;
-        base += W;
-        base_start = blast;
-    }
-}
-
 template <typename T, bool CM, bool EXACT, int V, int W, int OWN>
 __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
     constexpr int NSLOT = W * OWN;
@@ -494,22 +486,25 @@ __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
     if (e0l >= e1l) return;
     const int e0 = int(e0l), e1 = int(e1l);
     const int nbase = blockIdx.y * NSLOT * V;
+    // Split rows: the chunk's first row if it began before e0, its last row if it
+    // continues past e1 (COO row ids, no dependent row-offset loads).
+    const int first_row = __ldg(a.rows + e0), last_row = __ldg(a.rows + e1 - 1);
+    const bool first_split = e0 > 0 && __ldg(a.rows + e0 - 1) == first_row;
+    const bool last_split = e1 < a.nnz && __ldg(a.rows + e1) == last_row;
+    int prev_last = e0 > 0 ? __ldg(a.rows + e0 - 1) : -1;  // row of the element before the tile
 
-    int cur = a.chunk_row[w];
-    int cur_start = __ldg(a.rp + cur);
     for (int tb = e0; tb < e1; tb += W) {
         const int e = tb + gl;
         const bool valid = e < e1;
         const int c = valid ? ld_stream(a.ci + e) : 0;
         const T v = valid ? ld_stream(a.va + e) : T(0);
-        int row, rs, re;
-        resolve_rows<W>(mask, a.rp, a.M, e, valid, cur, cur_start, row, rs, re);
-        const int id = valid ? row : a.M;  // sentinel pads the tile (spmm.hpp:167)
-        const unsigned gates = scan_gates<W>(mask, id, gl);
-        const int prev_id = __shfl_up_sync(mask, id, 1, W);
-        const bool seg_start = valid && (gl == 0 || prev_id != id);
-        const bool owned = rs >= e0 && re <= e1;
-        const bool first = (e == rs);
+        const int row = valid ? ld_stream(a.rows + e) : a.M;  // sentinel pads (spmm.hpp:167)
+        const unsigned gates = scan_gates<W>(mask, row, gl);
+        const int prev_id = __shfl_up_sync(mask, row, 1, W);
+        const bool seg_start = valid && (gl == 0 || prev_id != row);
+        const int before = gl == 0 ? prev_last : prev_id;
+        const bool first = before != row;  // this segment opens its row
+        const bool owned = !((first_split && row == first_row) || (last_split && row == last_row));
 #pragma unroll
         for (int s0 = 0; s0 < NSLOT; s0 += U) {
             Frag<T, V> b[U];
@@ -550,8 +545,7 @@ __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
         }
         __syncwarp(mask);  // orders this tile's owned-row stores before the next tile's RMW
         const int last = min(W, e1 - tb) - 1;
-        cur = __shfl_sync(mask, row, last, W);
-        cur_start = __shfl_sync(mask, rs, last, W);
+        prev_last = __shfl_sync(mask, row, last, W);
     }
 }
 

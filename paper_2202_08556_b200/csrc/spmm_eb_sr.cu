@@ -51,35 +51,37 @@ cudaError_t launch_eb_sr<double>(const Plan& p, const SpmmArgs<double>& a, cudaS
 }
 
 template <typename T>
-cudaError_t launch_eb_prep_uniform(const int* rp, int M, int64_t nnz, int64_t sub, int64_t n_sub,
-                                   int G, int* chunk_row, T* C, int64_t ldc, int N,
-                                   const int* empty_rows, int n_empty, cudaStream_t s) {
+cudaError_t launch_eb_prep_uniform(const int* rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
+                                   T* C, int64_t ldc, int N, const int* empty_rows, int n_empty,
+                                   cudaStream_t s) {
     const int64_t work = n_sub + int64_t(n_empty) * N;
     if (work == 0) return cudaSuccess;
     const int64_t blocks = (work + kThreads - 1) / kThreads;
     k_eb_prep_uniform<T><<<dim3(unsigned(blocks)), kThreads, 0, s>>>(
-        rp, M, nnz, sub, n_sub, G, chunk_row, C, ldc, N, empty_rows, n_empty);
+        rows, nnz, sub, n_sub, G, C, ldc, N, empty_rows, n_empty);
     return cudaGetLastError();
 }
-template cudaError_t launch_eb_prep_uniform<float>(const int*, int, int64_t, int64_t, int64_t, int,
-                                                   int*, float*, int64_t, int, const int*, int,
+template cudaError_t launch_eb_prep_uniform<float>(const int*, int64_t, int64_t, int64_t, int,
+                                                   float*, int64_t, int, const int*, int,
                                                    cudaStream_t);
-template cudaError_t launch_eb_prep_uniform<double>(const int*, int, int64_t, int64_t, int64_t,
-                                                    int, int*, double*, int64_t, int, const int*,
-                                                    int, cudaStream_t);
+template cudaError_t launch_eb_prep_uniform<double>(const int*, int64_t, int64_t, int64_t, int,
+                                                    double*, int64_t, int, const int*, int,
+                                                    cudaStream_t);
 
 template <typename T>
 cudaError_t launch_eb_prep(const int* rp, int M, int64_t nnz, int64_t P, int* chunk_row, T* C,
-                           int64_t ldc, int N, const int* empty_rows, int n_empty, cudaStream_t s) {
+                           int64_t ldc, int N, const int* empty_rows, int n_empty,
+                           const int* rows, cudaStream_t s) {
     const int64_t work = P + int64_t(n_empty) * N;
     if (work == 0) return cudaSuccess;
     const int64_t blocks = (work + kThreads - 1) / kThreads;
     k_eb_prep<T><<<dim3(unsigned(blocks)), kThreads, 0, s>>>(rp, M, nnz, P, chunk_row, C, ldc, N,
-                                                             empty_rows, n_empty);
+                                                             empty_rows, n_empty, rows);
     return cudaGetLastError();
 }
 template cudaError_t launch_eb_prep<float>(const int*, int, int64_t, int64_t, int*, float*,
-                                           int64_t, int, const int*, int, cudaStream_t);
+                                           int64_t, int, const int*, int, const int*, cudaStream_t);
 template cudaError_t launch_eb_prep<double>(const int*, int, int64_t, int64_t, int*, double*,
-                                            int64_t, int, const int*, int, cudaStream_t);
+                                            int64_t, int, const int*, int, const int*,
+                                            cudaStream_t);
 }  // namespace daspmm
