@@ -28,19 +28,46 @@ struct Frag {
     T v[V];
 };
 
-// 128/64/32-bit vector gather of V consecutive elements (read-only path; B is
-// re-read across rows, so it keeps the default L2 policy).
+// L2 policy for B gathers: B rows are re-read by many rows of A, while A and C stream
+// through once (evict-first loads/stores), so B lines are marked evict-last.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// 128/64/32-bit vector gather of V consecutive elements of B (read-only path).
 template <typename T, int V>
 __device__ __forceinline__ Frag<T, V> ld_frag(const T* __restrict__ p) {
     Frag<T, V> f;
+#ifdef DASPMM_NO_L2_HINT
     if constexpr (V == 1) {
         f.v[0] = __ldg(p);
     } else {
         using VT = typename VecT<T, V>::type;
         const VT t = __ldg(reinterpret_cast<const VT*>(p));
-        static_assert(sizeof(VT) == sizeof(Frag<T, V>), "frag size");
         *reinterpret_cast<VT*>(f.v) = t;
     }
+#else
+    const uint64_t pol = policy_evict_last();
+    if constexpr (sizeof(T) == 4 && V == 4) {
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(f.v[0]), "=f"(f.v[1]), "=f"(f.v[2]), "=f"(f.v[3])
+                     : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 4 && V == 2) {
+        asm("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(f.v[0]), "=f"(f.v[1]) : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 4 && V == 1) {
+        asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+                     : "=f"(f.v[0]) : "l"(p), "l"(pol));
+    } else if constexpr (sizeof(T) == 8 && V == 2) {
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(f.v[0]), "=d"(f.v[1]) : "l"(p), "l"(pol));
+    } else {
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                     : "=d"(f.v[0]) : "l"(p), "l"(pol));
+    }
+#endif
     return f;
 }
 
