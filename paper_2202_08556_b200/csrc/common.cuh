@@ -28,8 +28,9 @@ struct Frag {
     T v[V];
 };
 
-// L2 policy for B gathers: B rows are re-read by many rows of A, while A and C stream
-// through once (evict-first loads/stores), so B lines are marked evict-last.
+// Optional L2 policy for B gathers (-DDASPMM_L2_HINT): mark B lines evict-last.
+// Measured on B200 (profiles/r01_notes.md): no gain over the default policy with A and
+// C already streaming evict-first, so it is off by default.
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -40,7 +41,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 template <typename T, int V>
 __device__ __forceinline__ Frag<T, V> ld_frag(const T* __restrict__ p) {
     Frag<T, V> f;
-#ifdef DASPMM_NO_L2_HINT
+#ifndef DASPMM_L2_HINT
     if constexpr (V == 1) {
         f.v[0] = __ldg(p);
     } else {
