@@ -114,16 +114,16 @@ def _dist():
 
 
 # ------------------------------------------------------------------ workload
-def build_suite(small: bool, rank: int, world: int):
-    """Generates the suite on the current device; returns per-matrix dicts holding the
-    rank's row panel as a DeviceCsr."""
+def build_suite(small: bool, rank: int, world: int, workload: str = "suite"):
+    """Generates the workload's matrices on the current device; returns per-matrix dicts
+    holding the rank's row panel as a DeviceCsr (and the N values to run)."""
     import torch
 
     from paper_2202_08556_b200 import gen, multi
     from paper_2202_08556_b200 import spmmkit as sk
 
     mats = []
-    for name, mk in gen.suite(small=small):
+    for name, mk, ns in gen.workload(workload, small=small):
         M, K, rp, ci, va = mk()
         full = sk.DeviceCsr.from_device(M, K, rp, ci, va)
         if world > 1:
@@ -134,7 +134,7 @@ def build_suite(small: bool, rank: int, world: int):
         else:
             r0, r1, d = 0, M, full
         mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), d=d, full=full,
-                         rows=(r0, r1), rp=rp, ci=ci, va=va))
+                         rows=(r0, r1), rp=rp, ci=ci, va=va, ns=ns))
     return mats
 
 
@@ -153,15 +153,16 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     sk.lib()  # fail loudly if the CUDA library is missing
     model = sk.load_selector(open(args.model).read())
-    mats = build_suite(args.small, rank, world)
+    mats = build_suite(args.small, rank, world, args.workload)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    ns = [int(n) for n in args.ns.split(",")] if args.ns else list(NS)
+    ns_override = [int(n) for n in args.ns.split(",")] if args.ns else None
+    ns = sorted({n for m in mats for n in (ns_override or m["ns"])})
 
     # Operands per (matrix, N): B replicated, C local panel.
     calls = []
     for m in mats:
         d = m["d"]
-        for n in ns:
+        for n in (ns_override or m["ns"]):
             B = gen.dense_operand(m["K"], n, seed=1000 + n, device=dev)
             Cp = torch.empty(d.num_rows, n, device=dev)
             kout = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -207,12 +208,13 @@ def run_ours(args):
         tt = torch.tensor([step_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms = float(tt.item())
-    total_flops = sum(gen.flops(m["nnz_total"], n) for m in mats for n in ns)
+    total_flops = sum(gen.flops(c["m"]["nnz_total"], c["n"]) for c in calls)
     value = total_flops / (step_ms * 1e-3) / 1e9
 
-    # kernel choices and launch count (select + [EB prologue] + spmm per call)
+    # kernel choices and launch count: after the warm-up every call's decision is
+    # published, so a timed call is [EB prologue] + the chosen kernel (no selector node)
     chosen = [int(c["kout"].item()) for c in calls]
-    launches_per_step = sum(2 + (1 if k >= 4 else 0) for k in chosen)
+    launches_per_step = sum(1 + (1 if k >= 4 else 0) for k in chosen)
 
     # roofline over this rank's calls
     peak, peak_kind = _peaks()
@@ -230,6 +232,21 @@ def run_ours(args):
         pass
 
     # ---- e2e: host operands through the public API (pinned H2D, DA-SpMM, D2H)
+    if sum(c["B"].numel() + c["C"].numel() for c in calls) * 4 > (16 << 30):
+        e2e = None  # operands too large to stage in pinned host memory (c5: 68 GB)
+    else:
+        e2e = _e2e(calls, one, stream, args, world, total_flops)
+    parity = _spot_check(calls[dom]) if rank == 0 else None
+    return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
+                   per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
+                   flush)
+
+
+def _e2e(calls, one, stream, args, world, total_flops):
+    import torch
+    import torch.distributed as dist
+
+    dev = calls[0]["B"].device
     hostB = [c["B"].cpu().pin_memory() for c in calls]
     hostC = [torch.empty(c["C"].shape, dtype=torch.float32).pin_memory() for c in calls]
     h2d = sum(b.numel() * 4 for b in hostB)
@@ -243,7 +260,7 @@ def run_ours(args):
 
     e2e_step()
     torch.cuda.synchronize()
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 3 if args.workload == "suite" else 1))
     if world > 1:
         dist.barrier()
     s = torch.cuda.Event(enable_timing=True)
@@ -259,24 +276,34 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_value = total_flops / (e2e_ms * 1e-3) / 1e9
+    return {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h}
 
-    # parity spot-check of the timed outputs against the fp64 CPU oracle (rows sample)
-    parity = _spot_check(calls[dom]) if rank == 0 else None
+
+def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
+            per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
+            flush):
+    import torch.distributed as dist
+
+    from paper_2202_08556_b200 import spmmkit as sk
 
     result = {
         "metric": "SpMM GFLOP/s (2*nnz*N/t), DA-SpMM over the synthetic suite",
         "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[1] synthetic suite: uniform/banded/power-law, "
-                               + ("2^14,2^17" if args.small else "2^14,2^17,2^20")
-                               + " rows, deg 16, N=" + ",".join(map(str, ns)),
+        "config": {"workload": ("configs[1] synthetic suite: uniform/banded/power-law, "
+                                + ("2^14,2^17" if args.small else "2^14,2^17,2^20")
+                                + " rows, deg 16, N=" + ",".join(map(str, ns)))
+                               if args.workload == "suite" else
+                               f"{args.workload}: " + ", ".join(
+                                   f'{m["name"]} M={m["M"]} nnz={m["nnz_total"]}' for m in mats)
+                               + " N=" + ",".join(map(str, ns)),
                    "matrices": [m["name"] for m in mats], "ns": ns,
                    "calls_per_step": len(calls), "selector": os.path.basename(args.model),
                    "l2": "flushed (256 MiB write) before every timed call",
                    "parallelism": f"row-panels x{world}, B replicated" if world > 1 else "1 GPU"},
-        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+        "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -297,7 +324,8 @@ def run_ours(args):
     if rank == 0 and not args.no_cusparse:
         result["cusparse"] = _cusparse_compare(calls, flush, per_call_ms, ns)
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = _cpu_baseline(mats, ns, steps=1)
+        result["cpu_baseline"] = _cpu_baseline(
+            mats, [int(n) for n in args.ns.split(",")] if args.ns else None, steps=1)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -315,14 +343,12 @@ def _spot_check(c):
     r0, r1 = m["rows"]
     rp = m["rp"].cpu().numpy().astype(np.int64)[r0:r1 + 1]
     rows = np.unique(np.linspace(0, r1 - r0 - 1, num=min(512, r1 - r0)).astype(np.int64))
-    ci = m["ci"].cpu().numpy().astype(np.int64)
-    va = m["va"].cpu().numpy().astype(np.float64)
     sub_rp = [0]
     sub_ci, sub_va = [], []
-    for r in rows:
-        s, e = rp[r], rp[r + 1]
-        sub_ci.append(ci[s:e])
-        sub_va.append(va[s:e])
+    for r in rows:  # slice on the device, copy only the sampled rows
+        s, e = int(rp[r]), int(rp[r + 1])
+        sub_ci.append(m["ci"][s:e].cpu().numpy().astype(np.int64))
+        sub_va.append(m["va"][s:e].cpu().numpy().astype(np.float64))
         sub_rp.append(sub_rp[-1] + (e - s))
     a = O.Csr(len(rows), m["K"], np.array(sub_rp), np.concatenate(sub_ci), np.concatenate(sub_va))
     x = c["B"].cpu().numpy().astype(np.float64)
@@ -365,8 +391,10 @@ def _cusparse_compare(calls, flush, our_ms, ns):
                             c["n"], out.data_ptr(), c["n"], alg, stream.cuda_stream,
                             C.byref(h)) != 0:
                 continue
-            for _ in range(2):
-                L.cmp_run(h)
+            if L.cmp_run(h) != 0:
+                L.cmp_destroy(h)
+                continue
+            L.cmp_run(h)
             samples = []
             for _ in range(3):
                 flush.zero_()
@@ -397,10 +425,28 @@ def _cusparse_compare(calls, flush, our_ms, ns):
 
 
 # ------------------------------------------------------------------ CPU reference
-def _ref_sample(mats, ns):
-    """The CPU reference's sample: every (matrix, N) pair of the suite (one pass is
-    ~30 GFLOP, a few seconds on the host's cores)."""
-    return [(m, n) for m in mats for n in ns]
+REF_PANEL_NNZ = 4_000_000
+
+
+def _ref_sample(mats, ns_override=None):
+    """The CPU reference's sample: every (matrix, N) pair of the workload. Matrices
+    above REF_PANEL_NNZ nonzeros are represented by a middle row panel of about that
+    many nonzeros (rows are independent in spmm, spmm.hpp:23-30, so a panel's
+    GFLOP/s is the matrix's), keeping one pass to a few seconds of CPU work."""
+    return [(m, n) for m in mats for n in (ns_override or m["ns"])]
+
+
+def _ref_panel(m):
+    import numpy as np
+
+    rp = m["rp"].cpu().numpy().astype(np.int64)
+    nnz = int(rp[-1])
+    if nnz <= REF_PANEL_NNZ:
+        return 0, m["M"]
+    mid = np.searchsorted(rp, nnz // 2)
+    r0 = int(np.searchsorted(rp, max(0, rp[mid] - REF_PANEL_NNZ // 2)))
+    r1 = int(np.searchsorted(rp, min(nnz, rp[r0] + REF_PANEL_NNZ)))
+    return r0, max(r1, r0 + 1)
 
 
 def _cpu_time_reference(sample, steps):
@@ -416,12 +462,16 @@ def _cpu_time_reference(sample, steps):
     handles = {}
     tot_flops = 0
     tot_s = 0.0
+    panel_nnz = {}
     for m, n in sample:
         if m["name"] not in handles:
+            r0, r1 = _ref_panel(m)
             rp = m["rp"].cpu().numpy().astype(np.int64)
-            ci = m["ci"].cpu().numpy().astype(np.int64)
-            va = m["va"].cpu().numpy().astype(np.float64)
-            handles[m["name"]] = R.ref_csr_from_csr(m["M"], m["K"], rp, ci, va)
+            s, e = int(rp[r0]), int(rp[r1])
+            ci = m["ci"][s:e].cpu().numpy().astype(np.int64)
+            va = m["va"][s:e].cpu().numpy().astype(np.float64)
+            handles[m["name"]] = R.ref_csr_from_csr(r1 - r0, m["K"], rp[r0:r1 + 1] - s, ci, va)
+            panel_nnz[m["name"]] = e - s
         h = handles[m["name"]]
         x = np.random.default_rng(n).uniform(-1, 1, (m["K"], n)).astype(np.float32).reshape(-1)
         med, mn, ck = C.c_double(), C.c_double(), C.c_double()
@@ -430,14 +480,14 @@ def _cpu_time_reference(sample, steps):
         if rc:
             raise RuntimeError(R.ref_last_error().decode())
         tot_s += med.value
-        tot_flops += 2 * m["nnz_total"] * n
+        tot_flops += 2 * panel_nnz[m["name"]] * n
     for h in handles.values():
         R.ref_csr_free(h)
     return tot_flops / tot_s / 1e9, cores, tot_s
 
 
-def _cpu_baseline(mats, ns, steps=1):
-    sample = _ref_sample(mats, ns)
+def _cpu_baseline(mats, ns_override=None, steps=1):
+    sample = _ref_sample(mats, ns_override)
     r = _cpu_time_reference(sample, steps)
     if r is None:
         return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
@@ -446,7 +496,8 @@ def _cpu_baseline(mats, ns, steps=1):
     return {"value": round(v, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
             "sample": f"reference spmm() RB+RM+SR fp32, P={cores} threads, time_kernel_fn "
                       f"(warmup 1, reps 3, median) over all {len(sample)} (matrix, N) pairs of the "
-                      f"suite; {secs:.2f} s of timed CPU work per pass"}
+                      f"workload (matrices > {REF_PANEL_NNZ} nnz as a middle row panel of that "
+                      f"size); {secs:.2f} s of timed CPU work per pass"}
 
 
 def run_reference(args):
@@ -463,10 +514,11 @@ def run_reference(args):
     from paper_2202_08556_b200 import gen
 
     mats = []
-    for name, mk in gen.suite(small=args.small, device=dev):
+    for name, mk, wns in gen.workload(args.workload, small=args.small, device=dev):
         M, K, rp, ci, va = mk()
-        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), rp=rp, ci=ci, va=va))
-    sample = _ref_sample(mats, ns)
+        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), rp=rp, ci=ci, va=va,
+                         ns=wns))
+    sample = _ref_sample(mats, [int(n) for n in args.ns.split(",")] if args.ns else None)
     from oracle import oracle as O
 
     if O.ref() is None:
@@ -481,14 +533,14 @@ def run_reference(args):
         vals.append(v)
         secs += s
     value = statistics.median(vals)
-    tot_flops = sum(2 * m["nnz_total"] * n for m, n in sample)
     out = {"impl": "reference",
            "metric": "SpMM GFLOP/s (2*nnz*N/t), DA-SpMM over the synthetic suite",
            "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(tot_flops / (value * 1e9) * 1e3, 3),
+           "warmup": args.warmup, "ms_per_step": round(secs / max(args.steps, 1) * 1e3, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic",
-           "config": {"workload": "configs[1] synthetic suite (bounded CPU sample)", "ns": ns},
+           "config": {"workload": f"{args.workload} (reference CPU; matrices above "
+                                  f"{REF_PANEL_NNZ} nnz as a middle row panel)", "ns": ns},
            "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
@@ -507,6 +559,8 @@ def main():
     ap.add_argument("--model", default=os.path.join(ROOT, "paper_2202_08556_b200", "models",
                                                     "b200_selector.txt"))
     ap.add_argument("--small", action="store_true", help="2^14 and 2^17 matrices only")
+    ap.add_argument("--workload", default="suite", choices=["suite", "c1", "c3", "c4", "c5"],
+                    help="BASELINE.json config (default: configs[1] suite, the headline)")
     ap.add_argument("--ns", default="")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")

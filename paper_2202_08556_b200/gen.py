@@ -102,8 +102,11 @@ def banded(rows: int, half_width: int, seed: int = 0, dtype=torch.float32, devic
 
 
 def reddit_like(seed: int = 7, dtype=torch.float32, device="cuda"):
-    """c3: M = K = 232,965 power-law graph, ~114.6M nnz (Reddit's size)."""
-    return rmat(18, 114_615_892, *GRAPH500, seed=seed, dtype=dtype, device=device, crop=232_965)
+    """c3: M = K = 232,965 power-law graph, ~114.6M nnz (Reddit's size, average degree
+    ~492). R-MAT (0.45, 0.22, 0.22, 0.11) at scale 18, cropped: the Graph500 skew would
+    ask row 0 for ~825K distinct columns out of 233K, this one for ~85K."""
+    return rmat(18, 114_615_892, 0.45, 0.22, 0.22, 0.11, seed=seed, dtype=dtype, device=device,
+                crop=232_965)
 
 
 def dense_operand(rows: int, cols: int, seed: int, dtype=torch.float32, device="cuda"):
@@ -127,6 +130,35 @@ def suite(device="cuda", dtype=torch.float32, small: bool = False):
                                                           device=device))
 
 
+def workload(name: str, device="cuda", dtype=torch.float32, small: bool = False):
+    """The BASELINE.json configs as (matrix name, generator, [N...]) lists.
+
+      suite  configs[1]: uniform / banded / power-law, 2^14..2^20 rows, N = 2..128
+      c1     configs[0]: uniform 4096 x 4096, ~1% density, N = 32
+      c3     configs[2]: Reddit-scale power-law graph (233K nodes, ~114.6M nnz), N = 128
+      c4     configs[3]: R-MAT scale 22 (Graph500 skew and a = 0.7), N = 16 and 64
+      c5     configs[4]: R-MAT scale 25 (~503M nnz), N = 256
+    """
+    ns_suite = [2, 4, 8, 16, 32, 64, 128]
+    if name == "suite":
+        return [(n, mk, ns_suite) for n, mk in suite(device=device, dtype=dtype, small=small)]
+    if name == "c1":
+        return [("c1_uniform4096_1pct", lambda: uniform(4096, 4096, 167_772, seed=1, dtype=dtype,
+                                                        device=device), [32])]
+    if name == "c3":
+        return [("c3_reddit_like", lambda: reddit_like(dtype=dtype, device=device), [128])]
+    if name == "c4":
+        s22 = 16 << 22
+        return [("c4_rmat_s22_graph500", lambda: rmat(22, s22, *GRAPH500, seed=22, dtype=dtype,
+                                                      device=device), [16, 64]),
+                ("c4_rmat_s22_a0.7", lambda: rmat(22, s22, 0.7, 0.1, 0.1, 0.1, seed=23, dtype=dtype,
+                                                  device=device), [16, 64])]
+    if name == "c5":
+        return [("c5_rmat_s25", lambda: rmat(25, 15 << 25, *GRAPH500, seed=25, dtype=dtype,
+                                             device=device), [256])]
+    raise ValueError(f"unknown workload {name}")
+
+
 def algorithmic_bytes(M: int, nnz: int, N: int, cols_touched: int, elem: int = 4,
                       off: int = 4) -> int:
     """off*(M+1) + 8*nnz + elem*N*K_touched + elem*N*M (int32 cols,
@@ -138,5 +170,5 @@ def flops(nnz: int, N: int) -> int:
     return 2 * nnz * N
 
 
-__all__ = ["rmat", "uniform", "banded", "reddit_like", "dense_operand", "suite",
+__all__ = ["rmat", "uniform", "banded", "reddit_like", "dense_operand", "suite", "workload",
            "algorithmic_bytes", "flops", "GRAPH500", "math"]
