@@ -279,15 +279,19 @@ __global__ void k_transpose(const T* __restrict__ in, int64_t rows, int64_t cols
                             T* __restrict__ out, int64_t ldo) {
     // in: rows x cols with leading dim ldi (row-major view); out: cols x rows, ldo.
     __shared__ T tile[32][33];
-    const int64_t bx = int64_t(blockIdx.x) * 32, by = int64_t(blockIdx.y) * 32;
-    for (int j = threadIdx.y; j < 32; j += 8) {
-        const int64_t r = by + j, c = bx + threadIdx.x;
-        if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * ldi + c];
-    }
-    __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += 8) {
-        const int64_t r = bx + j, c = by + threadIdx.x;  // out row = in col
-        if (r < cols && c < rows) out[r * ldo + c] = tile[threadIdx.x][j];
+    const int64_t bx = int64_t(blockIdx.x) * 32;
+    // Row tiles are strided over grid.y (which is capped at 65535).
+    for (int64_t by = int64_t(blockIdx.y) * 32; by < rows; by += int64_t(gridDim.y) * 32) {
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int64_t r = by + j, c = bx + threadIdx.x;
+            if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * ldi + c];
+        }
+        __syncthreads();
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int64_t r = bx + j, c = by + threadIdx.x;  // out row = in col
+            if (r < cols && c < rows) out[r * ldo + c] = tile[threadIdx.x][j];
+        }
+        __syncthreads();
     }
 }
 
@@ -316,8 +320,10 @@ __global__ void k_debug_cond(const double* in, const int64_t* ids, double* out, 
 
 cudaError_t transpose(int dtype, const void* in, int64_t rows, int64_t cols, int64_t ldi,
                       void* out, int64_t ldo, cudaStream_t s) {
-    dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
     if (rows == 0 || cols == 0) return cudaSuccess;
+    if ((cols + 31) / 32 > 0x7fffffff) return cudaErrorInvalidValue;
+    dim3 grid(unsigned((cols + 31) / 32), unsigned(std::min<int64_t>((rows + 31) / 32, 65535))),
+        block(32, 8);
     if (dtype == DASPMM_F64)
         k_transpose<double><<<grid, block, 0, s>>>(static_cast<const double*>(in), rows, cols, ldi,
                                                    static_cast<double*>(out), ldo);

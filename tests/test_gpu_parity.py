@@ -381,3 +381,27 @@ def test_row_panels_reassemble_exactly(sk):
             pieces.append(Cp)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(torch.cat(pieces).cpu().numpy(), full.cpu().numpy())
+
+
+def test_auto_layout_tall_operand(sk):
+    """B with K > 2M rows: the device transpose must stride its row tiles (grid.y cap)."""
+    import torch
+
+    K = 2_300_000
+    rng = np.random.default_rng(9)
+    rows = 300
+    lens = rng.integers(0, 20, rows)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(K, size=l, replace=False)) for l in lens]).astype(np.int64)
+    a = sk.CsrMatrix(rows, K, rp, ci, rng.uniform(-1, 1, ci.size).astype(np.float32), np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    x = rng.uniform(-1, 1, (K, 2)).astype(np.float32)
+    B = torch.from_numpy(x).cuda()
+    Cc = torch.empty(rows, 2, device="cuda")
+    from paper_2202_08556_b200 import _lib
+
+    _lib.check(_lib.lib().daspmm_spmm_auto_layout(d._h, 2, 0, 8, 8, B.data_ptr(), 0, 2, 2,
+                                                  Cc.data_ptr(), 2, 0, None))
+    torch.cuda.synchronize()
+    y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+    assert (np.abs(Cc.cpu().numpy() - y64) <= H.gamma_bound(a, x, np.float32)).all()

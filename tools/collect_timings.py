@@ -35,6 +35,10 @@ def corpus(quick: bool):
         if not quick and s in (12, 16, 20):
             specs.append(("banded", s, 4, None))
             specs.append(("banded", s, 32, None))
+        if not quick and s in (11, 12, 13, 14):  # small, denser matrices (c1-like: 4096^2, 1%)
+            for deg in (40, 128):
+                specs.append(("uniform", s, deg, None))
+                specs.append(("rmat", s, deg, 0.45))
     for kind, s, deg, a in specs:
         seed = int(rng.integers(1 << 30))
         n = 1 << s
