@@ -130,6 +130,17 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     p.exact = exact;
     const bool eb = kernel >= 4, pr = kernel & 1;
     p.V = (p.cm || exact) ? 1 : pick_v(h->dtype, N, B, ldb, C, ldc);
+    // Small calls (few rows / nonzeros) cannot fill 148 SMs with one V-wide slot per
+    // lane: trade vector width for lanes until there are >= 2 CTAs per SM.
+    if (!pr) {
+        const int64_t units = eb ? std::max<int64_t>(h->nnz / 32, 1) : std::max<int64_t>(h->M, 1);
+        while (p.V > 1) {
+            const int64_t lanes_now = std::min<int64_t>(32, (N + p.V - 1) / p.V);
+            if (units * lanes_now >= 148LL * 512) break;  // >= 2 CTAs per SM
+            if ((N + p.V / 2 - 1) / (p.V / 2) > 64) break;  // keep <= 2 slots per lane
+            p.V /= 2;
+        }
+    }
     const int64_t ncols = std::min<int64_t>(N, max_tile_cols(h, N));
     const int64_t nv = (ncols + p.V - 1) / p.V;  // column slots per tile
     int64_t tile_cols;

@@ -42,12 +42,13 @@ def main():
     ap.add_argument("--only", default="", help="comma list of suite matrix names")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-torch", action="store_true")
+    ap.add_argument("--workload", default="suite")
     a = ap.parse_args()
     ns = [int(x) for x in a.ns.split(",")]
     ks = [int(x) for x in a.kernels.split(",")]
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     only = set(a.only.split(",")) if a.only else None
-    for name, mk in gen.suite(small=a.small):
+    for name, mk, _ in gen.workload(a.workload, small=a.small):
         if only and name not in only:
             continue
         M, K, rp, ci, va = mk()
