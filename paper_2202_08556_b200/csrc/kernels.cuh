@@ -71,12 +71,12 @@ __device__ __forceinline__ Frag<T, V> gather(const SpmmArgs<T>& a, int k, int co
 // group after it.
 template <typename T>
 struct CtaSlots {
-    T* L;      // [(G+1) * TN]
-    T* R;      // [(G+1) * TN]
-    int* row;  // [G+1], -1 when no row crosses the boundary
-    int g;     // this group's index in the CTA
-    int tile0; // first column of the CTA's column tile
-    int tn;    // tile width
+    T* L = nullptr;      // [(G+1) * TN]
+    T* R = nullptr;      // [(G+1) * TN]
+    int* row = nullptr;  // [G+1], -1 when no row crosses the boundary
+    int g = 0;           // this group's index in the CTA
+    int tile0 = 0;       // first column of the CTA's column tile
+    int tn = 0;          // tile width
 };
 
 enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2 };
@@ -84,7 +84,7 @@ enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2 };
 template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE>
 __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, const int e1, int r,
                                         const int nrows, const int n0, const unsigned mask,
-                                        const int gl, const CtaSlots<T>* slots = nullptr) {
+                                        const int gl, const CtaSlots<T> slots = CtaSlots<T>{}) {
     constexpr bool EB = MODE != kRB;
     constexpr int STEP = LPR >= 16 ? LPR : (LPR >= 4 ? 16 : 8);  // pairs per group per step
     constexpr int EPL = STEP / LPR;                              // pairs per lane per step
@@ -135,11 +135,11 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
             const int col = n0 + s * LPR * V;
             if constexpr (MODE == kEBCta) {
                 if (!owned) {  // boundary piece -> shared slot, combined by the CTA
-                    const int b = head ? slots->g : slots->g + 1;
-                    T* dst = (head ? slots->R : slots->L) + b * slots->tn + (col - slots->tile0);
+                    const int b = head ? slots.g : slots.g + 1;
+                    T* dst = (head ? slots.R : slots.L) + b * slots.tn + (col - slots.tile0);
 #pragma unroll
                     for (int i = 0; i < V; ++i) dst[i] = out.v[i];
-                    if (s == 0 && gl == 0) slots->row[b] = r;
+                    if (s == 0 && gl == 0) slots.row[b] = r;
                     continue;
                 }
             }
@@ -300,11 +300,13 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
 k_eb_sr_cta(const SpmmArgs<T> a) {
     constexpr int G = kThreads / LPR;
     constexpr int TN = LPR * V * CPL;
-    __shared__ T sL[(G + 1) * TN];
-    __shared__ T sR[(G + 1) * TN];
-    __shared__ int srow[G + 1];
-    for (int i = threadIdx.x; i < (G + 1) * TN; i += kThreads) sL[i] = sR[i] = T(0);
-    for (int i = threadIdx.x; i < G + 1; i += kThreads) srow[i] = -1;
+    // +1 padding: ptxas pairs the combine loop's loads into 64-bit LDS, and with an odd
+    // trip count (G + 1) the last pair would read one element past the array.
+    __shared__ T sL[(G + 2) * TN];
+    __shared__ T sR[(G + 2) * TN];
+    __shared__ int srow[G + 2];
+    for (int i = threadIdx.x; i < (G + 2) * TN; i += kThreads) sL[i] = sR[i] = T(0);
+    for (int i = threadIdx.x; i < G + 2; i += kThreads) srow[i] = -1;
     __syncthreads();
 
     const unsigned mask = group_mask<LPR>();
@@ -319,7 +321,7 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
     CtaSlots<T> slots{sL, sR, srow, g, tile0, TN};
     if (e0 < e1)
         sr_walk<T, CM, false, V, LPR, CPL, kEBCta>(a, int(e0), int(e1), __ldg(a.rows + e0), 0, n0,
-                                                   mask, gl, &slots);
+                                                   mask, gl, slots);
     __syncthreads();
     // Combine: thread t owns tile column t; boundaries in order, segmented by row.
     for (int t = threadIdx.x; t < TN; t += kThreads) {

@@ -317,6 +317,12 @@ def _stream_ptr(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
+def _ld(t) -> int:
+    """Leading dimension of a row-major 2-D tensor (torch ignores the stride of a
+    size-1 dimension when deciding contiguity, so do not trust it there)."""
+    return int(t.stride(0)) if t.shape[0] > 1 else int(max(t.shape[1], 1))
+
+
 def _as_device(a) -> DeviceCsr:
     return a if isinstance(a, DeviceCsr) else DeviceCsr.from_host(a)
 
@@ -366,12 +372,9 @@ def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int 
     kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
     if b_layout is None:
         b_layout = Layout.ColMajor if (kid >> 1) & 1 else Layout.RowMajor
-    if b_layout == Layout.RowMajor:
-        n, ldb = B.shape[1], B.stride(0)
-    else:
-        n, ldb = B.shape[0], B.stride(0)
-    check(lib().daspmm_spmm(a._h, kid, P, W, Cb, B.data_ptr(), int(b_layout), ldb, n,
-                            C_out.data_ptr(), C_out.stride(0), _lib.EXACT if exact else 0,
+    n = B.shape[1] if b_layout == Layout.RowMajor else B.shape[0]
+    check(lib().daspmm_spmm(a._h, kid, P, W, Cb, B.data_ptr(), int(b_layout), _ld(B), n,
+                            C_out.data_ptr(), _ld(C_out), _lib.EXACT if exact else 0,
                             _stream_ptr(stream)))
     return C_out
 
@@ -459,13 +462,10 @@ def select_device(a: DeviceCsr, model: SelectorModel, n_cols: int, out, hw: int 
 def spmm_selected(a: DeviceCsr, model: SelectorModel, B, C_out, b_layout=Layout.RowMajor,
                   W: int = 8, hw: int = -1, exact: bool = False, kernel_out=None, stream=None):
     """DA-SpMM: device selector + on-device dispatch (graph SWITCH node)."""
-    if b_layout == Layout.RowMajor:
-        n, ldb = B.shape[1], B.stride(0)
-    else:
-        n, ldb = B.shape[0], B.stride(0)
+    n = B.shape[1] if b_layout == Layout.RowMajor else B.shape[0]
     kp = kernel_out.data_ptr() if kernel_out is not None else None
-    check(lib().daspmm_spmm_selected(a._h, model._m, hw, B.data_ptr(), int(b_layout), ldb, n,
-                                     C_out.data_ptr(), C_out.stride(0), W,
+    check(lib().daspmm_spmm_selected(a._h, model._m, hw, B.data_ptr(), int(b_layout), _ld(B), n,
+                                     C_out.data_ptr(), _ld(C_out), W,
                                      _lib.EXACT if exact else 0, kp, _stream_ptr(stream)))
     return C_out
 

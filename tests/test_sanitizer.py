@@ -1,0 +1,28 @@
+"""compute-sanitizer memcheck + racecheck over every kernel (8 design points, fast and
+exact, f32 and f64, W 4/32) plus the selector and graph dispatch (tools/sanitize.py)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize.py")], capture_output=True,
+                       text=True, timeout=900, cwd=ROOT)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "sanitize driver done" in r.stdout, tail

@@ -1,0 +1,35 @@
+"""compute-sanitizer driver: every kernel (8 design points x fast/exact, f32/f64) plus
+the selector and graph dispatch on small skewed inputs. Run under
+compute-sanitizer --tool {memcheck,racecheck,synccheck}."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import helpers as H  # noqa: E402
+from paper_2202_08556_b200 import spmmkit as sk  # noqa: E402
+
+model = sk.load_selector(open(os.path.join(os.path.dirname(sk.__file__), "models",
+                                           "b200_selector.txt")).read())
+for dtype in (np.float32, np.float64):
+    a = H.random_csr(700, 600, 9000, seed=4, dtype=dtype, skew=1.4)
+    d = sk.DeviceCsr.from_host(a)
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    for n in (1, 3, 8, 33, 128):
+        B = torch.rand(600, n, dtype=tdt, device="cuda")
+        Bcm = B.t().contiguous()
+        C = torch.empty(700, n, dtype=tdt, device="cuda")
+        for k in range(8):
+            for exact in (False, True):
+                for W in (4, 32):
+                    sk.spmm_device(k, d, Bcm if k & 2 else B, C, W=W, P=(64 if exact else 0),
+                                   exact=exact)
+        if dtype == np.float32:
+            kout = torch.zeros(1, dtype=torch.int32, device="cuda")
+            sk.spmm_selected(d, model, B, C, kernel_out=kout)
+            sk.spmm_selected(d, model, B, C, kernel_out=kout)
+torch.cuda.synchronize()
+print("sanitize driver done")
