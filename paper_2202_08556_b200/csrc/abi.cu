@@ -164,7 +164,14 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         const int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
         p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);
         workers = p.P;
-        if (!pr && !exact && P <= 0) {  // fast path: CTA-combined boundary rows
+        if (!pr && !exact && P <= 0 && p.L == 1 && p.X == 1 && N <= p.V && !p.cm &&
+            h->dtype == DASPMM_F32) {
+            // one-lane groups: CTA-staged thread sub-chunks (k_eb_sr_thr)
+            p.thr = true;
+            p.sub = p.V >= 4 ? 8 : 15;  // 3 x sub x 257 x 4 B of staging < 48 KB
+            p.P = (h->nnz + p.sub - 1) / p.sub;
+            workers = p.P;
+        } else if (!pr && !exact && P <= 0) {  // fast path: CTA-combined boundary rows
             p.cta = true;
             p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
             p.sub = std::max<int64_t>(p.sub, 1);
@@ -223,7 +230,9 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if (eb) {
         cudaError_t e =
-            p.cta ? launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, kThreads / p.L,
+            (p.cta || p.thr)
+                  ? launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P,
+                                              p.thr ? 1 : kThreads / p.L,
                                               static_cast<T*>(C), ldc, int(N), h->empty_rows,
                                               int(h->n_empty), s)
                   : launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,

@@ -21,6 +21,7 @@ struct Plan {
     int64_t P = 0;       // EB chunks
     int64_t rpg = 1;     // RB+SR rows per group (row-block size)
     bool cta = false;    // EB+SR fast path: CTA-combined boundary rows (k_eb_sr_cta)
+    bool thr = false;    // EB+SR fast path for one-lane groups: staged sub-chunks (k_eb_sr_thr)
     int64_t sub = 0;     // ... its pairs per group sub-chunk
 };
 

@@ -350,6 +350,72 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
     }
 }
 
+// EB + SR, fast path for one-lane groups (N <= V, i.e. N <= 4 in fp32): every thread
+// owns a sub-chunk of S pairs. The CTA first stages its contiguous range of (col, val,
+// row id) into shared memory with coalesced loads, transposed (pair i of thread t at
+// [i][t], row pitch 257 — conflict-free for both the staging stores and the per-thread
+// reads); each thread then issues all S of its B gathers before accumulating, so a
+// warp keeps 32*S gathers in flight. Owned rows are stored, rows cut by a sub-chunk
+// boundary take atomics (pre-zeroed by k_eb_prep_uniform with G = 1).
+template <typename T, bool CM, int V, int S>
+__global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) {
+    constexpr int PITCH = kThreads + 1;
+    __shared__ int s_c[S * PITCH];
+    __shared__ int s_r[S * PITCH];
+    __shared__ T s_v[S * PITCH];
+    const int64_t E0 = int64_t(blockIdx.x) * kThreads * S;
+    const int64_t E1 = min(a.nnz, E0 + int64_t(kThreads) * S);
+    for (int jj = threadIdx.x; jj < kThreads * S; jj += kThreads) {
+        const int64_t e = E0 + jj;
+        const int slot = (jj % S) * PITCH + jj / S;
+        const bool ok = e < E1;
+        s_c[slot] = ok ? ld_stream(a.ci + e) : 0;
+        s_v[slot] = ok ? ld_stream(a.va + e) : T(0);
+        s_r[slot] = ok ? ld_stream(a.rows + e) : INT_MAX;
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int64_t e0 = E0 + int64_t(t) * S;
+    const int64_t e1 = min(E1, e0 + S);
+    if (e0 >= e1) return;
+    const int n = int(e1 - e0);
+    const int col0 = blockIdx.y * V;  // one V-wide column slot per thread
+    Frag<T, V> b[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? s_c[i * PITCH + t] : 0, col0);
+    const int first_row = s_r[t];
+    const int last_row = s_r[(n - 1) * PITCH + t];
+    const int before = e0 == 0 ? -1 : (t > 0 ? s_r[(S - 1) * PITCH + t - 1] : __ldg(a.rows + e0 - 1));
+    const int after = e1 >= a.nnz ? -1
+                      : (e1 < E1 ? s_r[t + 1] : __ldg(a.rows + e1));
+    const bool first_split = before == first_row, last_split = after == last_row;
+    Frag<T, V> acc;
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc.v[i] = T(0);
+    int r = first_row;
+    auto flush = [&]() {
+        T* y = a.C + int64_t(r) * a.ldc + col0;
+        if ((first_split && r == first_row) || (last_split && r == last_row)) atomic_add_frag(y, acc);
+        else st_frag(y, acc);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc.v[i] = T(0);
+    };
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        if (i < n) {
+            const int rid = s_r[i * PITCH + t];
+            if (rid != r) {
+                flush();
+                r = rid;
+            }
+            const T v = s_v[i * PITCH + t];
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc.v[q] = madd<false>(acc.v[q], v, b[i].v[q]);
+        }
+    }
+    flush();
+}
+
 // Prologue of the EB fast path: uniform sub-chunks of `sub` pairs; chunk_row for every
 // sub-chunk (row of its first pair, by binary search), split-row zeroing only at CTA
 // boundaries (every G-th sub-chunk), empty rows from the handle's list.

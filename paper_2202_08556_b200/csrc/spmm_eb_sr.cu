@@ -41,8 +41,19 @@ cudaError_t launch_eb_sr_per_chunk(const Plan&, const SpmmArgs<T>&, cudaStream_t
 DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
 #undef launch_eb_sr
 
+static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    switch (p.V) {
+        case 1: k_eb_sr_thr<float, false, 1, 15><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 2: k_eb_sr_thr<float, false, 2, 15><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 4: k_eb_sr_thr<float, false, 4, 8><<<p.grid, kThreads, 0, s>>>(a); break;
+        default: return cudaErrorNotSupported;
+    }
+    return cudaGetLastError();
+}
+
 template <>
 cudaError_t launch_eb_sr<float>(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.thr) return launch_eb_sr_thr(p, a, s);
     return p.cta ? launch_eb_sr_cta<float>(p, a, s) : launch_eb_sr_per_chunk<float>(p, a, s);
 }
 template <>
