@@ -375,28 +375,36 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
     }
     __syncthreads();
     const int t = threadIdx.x;
+    const int lane = t & 31;
     const int64_t e0 = E0 + int64_t(t) * S;
     const int64_t e1 = min(E1, e0 + S);
-    if (e0 >= e1) return;
-    const int n = int(e1 - e0);
+    const bool active = e0 < e1;  // no early exit: the warp combines split rows below
+    const int n = active ? int(e1 - e0) : 0;
     const int col0 = blockIdx.y * V;  // one V-wide column slot per thread
     Frag<T, V> b[S];
 #pragma unroll
     for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? s_c[i * PITCH + t] : 0, col0);
-    const int first_row = s_r[t];
-    const int last_row = s_r[(n - 1) * PITCH + t];
-    const int before = e0 == 0 ? -1 : (t > 0 ? s_r[(S - 1) * PITCH + t - 1] : __ldg(a.rows + e0 - 1));
-    const int after = e1 >= a.nnz ? -1
+    const int first_row = active ? s_r[t] : INT_MAX;
+    const int last_row = active ? s_r[(n - 1) * PITCH + t] : INT_MAX;
+    const int before = !active || e0 == 0 ? -1
+                       : (t > 0 ? s_r[(S - 1) * PITCH + t - 1] : __ldg(a.rows + e0 - 1));
+    const int after = !active || e1 >= a.nnz ? -1
                       : (e1 < E1 ? s_r[t + 1] : __ldg(a.rows + e1));
-    const bool first_split = before == first_row, last_split = after == last_row;
-    Frag<T, V> acc;
+    const bool first_split = active && before == first_row;
+    const bool last_split = active && after == last_row;
+    // A split row's partial is parked (head = first row, tail = last row when distinct).
+    Frag<T, V> acc, head, tail;
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc.v[i] = T(0);
+    for (int i = 0; i < V; ++i) acc.v[i] = head.v[i] = tail.v[i] = T(0);
     int r = first_row;
     auto flush = [&]() {
-        T* y = a.C + int64_t(r) * a.ldc + col0;
-        if ((first_split && r == first_row) || (last_split && r == last_row)) atomic_add_frag(y, acc);
-        else st_frag(y, acc);
+        if (first_split && r == first_row) {
+            head = acc;
+        } else if (last_split && r == last_row) {
+            tail = acc;
+        } else {
+            st_frag(a.C + int64_t(r) * a.ldc + col0, acc);
+        }
 #pragma unroll
         for (int i = 0; i < V; ++i) acc.v[i] = T(0);
     };
@@ -413,7 +421,27 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
             for (int q = 0; q < V; ++q) acc.v[q] = madd<false>(acc.v[q], v, b[i].v[q]);
         }
     }
-    flush();
+    if (active) flush();
+    // Warp combine: the row crossing the boundary into lane l is lane l's first row; it
+    // collects lane l's head and lane l-1's tail, and runs of lanes lying wholly inside
+    // one long row share that key, so a gated scan sums each run into its first lane.
+    const bool has_tail = last_split && !(first_split && first_row == last_row);
+    const bool tail_in = __shfl_up_sync(kFull, has_tail ? 1 : 0, 1) && lane > 0;
+    const int key = first_split ? first_row : -1 - lane;  // unique keys for non-contributors
+    const unsigned gates = scan_gates<32>(kFull, key, lane);
+    const int prev_key = __shfl_up_sync(kFull, key, 1);
+    const bool seg_start = first_split && (lane == 0 || prev_key != key);
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+        const T tin = __shfl_up_sync(kFull, tail.v[q], 1);
+        T v = first_split ? head.v[q] + (tail_in ? tin : T(0)) : T(0);
+        v = group_conditional_scan_gated<32>(kFull, v, gates);
+        head.v[q] = v;
+    }
+    if (seg_start) atomic_add_frag(a.C + int64_t(first_row) * a.ldc + col0, head);
+    // tails with no receiving lane: the warp's last lane, or a receiver-less boundary
+    const bool tail_out = has_tail && (lane == 31 || !__shfl_down_sync(kFull, first_split, 1));
+    if (tail_out) atomic_add_frag(a.C + int64_t(last_row) * a.ldc + col0, tail);
 }
 
 // Prologue of the EB fast path: uniform sub-chunks of `sub` pairs; chunk_row for every
