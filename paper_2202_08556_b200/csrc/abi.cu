@@ -132,7 +132,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     p.V = (p.cm || exact) ? 1 : pick_v(h->dtype, N, B, ldb, C, ldc);
     // Small calls (few rows / nonzeros) cannot fill 148 SMs with one V-wide slot per
     // lane: trade vector width for lanes until there are >= 2 CTAs per SM.
-    if (!pr) {
+    // (EB+SR with N <= 4 keeps V = N: it runs the staged one-lane path instead.)
+    if (!pr && !(eb && !exact && N <= p.V && N <= 4)) {
         const int64_t units = eb ? std::max<int64_t>(h->nnz / 32, 1) : std::max<int64_t>(h->M, 1);
         while (p.V > 1) {
             const int64_t lanes_now = std::min<int64_t>(32, (N + p.V - 1) / p.V);

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
     // collects lane l's head and lane l-1's tail, and runs of lanes lying wholly inside
     // one long row share that key, so a gated scan sums each run into its first lane.
     const bool has_tail = last_split && !(first_split && first_row == last_row);
-    const bool tail_in = __shfl_up_sync(kFull, has_tail ? 1 : 0, 1) && lane > 0;
+    const bool tail_in = (__shfl_up_sync(kFull, has_tail ? 1 : 0, 1) != 0) && lane > 0;
     const int key = first_split ? first_row : -1 - lane;  // unique keys for non-contributors
     const unsigned gates = scan_gates<32>(kFull, key, lane);
     const int prev_key = __shfl_up_sync(kFull, key, 1);
@@ -439,8 +439,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
         head.v[q] = v;
     }
     if (seg_start) atomic_add_frag(a.C + int64_t(first_row) * a.ldc + col0, head);
-    // tails with no receiving lane: the warp's last lane, or a receiver-less boundary
-    const bool tail_out = has_tail && (lane == 31 || !__shfl_down_sync(kFull, first_split, 1));
+    // tails with no receiving lane: the warp's last lane, or a receiver-less boundary.
+    // (The shuffle runs on every lane — inside a short-circuit it would not.)
+    const bool next_takes = __shfl_down_sync(kFull, first_split ? 1 : 0, 1) != 0;
+    const bool tail_out = has_tail && (lane == 31 || !next_takes);
     if (tail_out) atomic_add_frag(a.C + int64_t(last_row) * a.ldc + col0, tail);
 }
 
