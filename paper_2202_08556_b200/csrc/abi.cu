@@ -169,7 +169,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             h->dtype == DASPMM_F32) {
             // one-lane groups: CTA-staged thread sub-chunks (k_eb_sr_thr)
             p.thr = true;
-            p.sub = p.V >= 4 ? 8 : 15;  // 3 x sub x 257 x 4 B of staging < 48 KB
+            p.sub = p.V >= 4 ? 7 : 15;  // odd; 3 x sub x 256 x 4 B of staging < 48 KB
             p.P = (h->nnz + p.sub - 1) / p.sub;
             workers = p.P;
         } else if (!pr && !exact && P <= 0) {  // fast path: CTA-combined boundary rows
@@ -233,7 +233,7 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
         cudaError_t e =
             (p.cta || p.thr)
                   ? launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P,
-                                              p.thr ? 1 : kThreads / p.L,
+                                              p.thr ? 32 : kThreads / p.L,
                                               static_cast<T*>(C), ldc, int(N), h->empty_rows,
                                               int(h->n_empty), s)
                   : launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,

@@ -160,7 +160,8 @@ __device__ __forceinline__ unsigned group_mask() {
 
 template <int G, typename T>
 __device__ __forceinline__ T gshfl(unsigned mask, T v, int src) {
-    return __shfl_sync(mask, v, src, G);
+    if constexpr (G == 1) return v;  // a one-lane group owns its value
+    else return __shfl_sync(mask, v, src, G);
 }
 
 // Adjacent-pair merge tree over the G lanes of a group — reduce.hpp:18-25.

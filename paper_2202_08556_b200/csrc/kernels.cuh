@@ -359,19 +359,31 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
 // boundary take atomics (pre-zeroed by k_eb_prep_uniform with G = 1).
 template <typename T, bool CM, int V, int S>
 __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) {
-    constexpr int PITCH = kThreads + 1;
-    __shared__ int s_c[S * PITCH];
-    __shared__ int s_r[S * PITCH];
-    __shared__ T s_v[S * PITCH];
+    static_assert(S % 2 == 1, "odd S keeps the per-thread strided reads conflict-free");
+    constexpr int PITCH = 1;  // natural order: pair i of thread t at [t*S + i]
+    __shared__ int s_c[S * kThreads];
+    __shared__ int s_r[S * kThreads];
+    __shared__ T s_v[S * kThreads];
     const int64_t E0 = int64_t(blockIdx.x) * kThreads * S;
     const int64_t E1 = min(a.nnz, E0 + int64_t(kThreads) * S);
-    for (int jj = threadIdx.x; jj < kThreads * S; jj += kThreads) {
-        const int64_t e = E0 + jj;
-        const int slot = (jj % S) * PITCH + jj / S;
-        const bool ok = e < E1;
-        s_c[slot] = ok ? ld_stream(a.ci + e) : 0;
-        s_v[slot] = ok ? ld_stream(a.va + e) : T(0);
-        s_r[slot] = ok ? ld_stream(a.rows + e) : INT_MAX;
+    {  // coalesced staging; every load of the tile is issued before any store
+        int lc[S], lr[S];
+        T lv[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const int64_t e = E0 + k * kThreads + threadIdx.x;
+            const bool ok = e < E1;
+            lc[k] = ok ? ld_stream(a.ci + e) : 0;
+            lv[k] = ok ? ld_stream(a.va + e) : T(0);
+            lr[k] = ok ? ld_stream(a.rows + e) : INT_MAX;
+        }
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const int jj = k * kThreads + threadIdx.x;
+            s_c[jj] = lc[k];
+            s_v[jj] = lv[k];
+            s_r[jj] = lr[k];
+        }
     }
     __syncthreads();
     const int t = threadIdx.x;
@@ -383,13 +395,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
     const int col0 = blockIdx.y * V;  // one V-wide column slot per thread
     Frag<T, V> b[S];
 #pragma unroll
-    for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? s_c[i * PITCH + t] : 0, col0);
-    const int first_row = active ? s_r[t] : INT_MAX;
-    const int last_row = active ? s_r[(n - 1) * PITCH + t] : INT_MAX;
+    for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? s_c[t * S + i] : 0, col0);
+    const int first_row = active ? s_r[t * S] : INT_MAX;
+    const int last_row = active ? s_r[t * S + n - 1] : INT_MAX;
     const int before = !active || e0 == 0 ? -1
-                       : (t > 0 ? s_r[(S - 1) * PITCH + t - 1] : __ldg(a.rows + e0 - 1));
+                       : (t > 0 ? s_r[t * S - 1] : __ldg(a.rows + e0 - 1));
     const int after = !active || e1 >= a.nnz ? -1
-                      : (e1 < E1 ? s_r[t + 1] : __ldg(a.rows + e1));
+                      : (e1 < E1 ? s_r[(t + 1) * S] : __ldg(a.rows + e1));
     const bool first_split = active && before == first_row;
     const bool last_split = active && after == last_row;
     // A split row's partial is parked (head = first row, tail = last row when distinct).
@@ -411,12 +423,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
 #pragma unroll
     for (int i = 0; i < S; ++i) {
         if (i < n) {
-            const int rid = s_r[i * PITCH + t];
+            const int rid = s_r[t * S + i];
             if (rid != r) {
                 flush();
                 r = rid;
             }
-            const T v = s_v[i * PITCH + t];
+            const T v = s_v[t * S + i];
 #pragma unroll
             for (int q = 0; q < V; ++q) acc.v[q] = madd<false>(acc.v[q], v, b[i].v[q]);
         }
@@ -438,10 +450,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
         v = group_conditional_scan_gated<32>(kFull, v, gates);
         head.v[q] = v;
     }
-    if (seg_start) atomic_add_frag(a.C + int64_t(first_row) * a.ldc + col0, head);
-    // tails with no receiving lane: the warp's last lane, or a receiver-less boundary.
-    // (The shuffle runs on every lane — inside a short-circuit it would not.)
+    // A run that neither began before the warp's range (lane 0's head) nor continues
+    // past it (lane 31 wholly inside the row) is complete: plain store. Only rows that
+    // cross a warp boundary take atomics (pre-zeroed at warp granularity).
+    // (Shuffles run on every lane — inside a short-circuit they would not.)
     const bool next_takes = __shfl_down_sync(kFull, first_split ? 1 : 0, 1) != 0;
+    const int l31_key = __shfl_sync(kFull, key, 31);
+    const bool l31_cont = __shfl_sync(kFull, (last_split && first_row == last_row) ? 1 : 0, 31);
+    if (seg_start) {
+        T* y = a.C + int64_t(first_row) * a.ldc + col0;
+        const bool crosses = lane == 0 || (l31_key == key && l31_cont);
+        if (crosses) atomic_add_frag(y, head);
+        else st_frag(y, head);
+    }
     const bool tail_out = has_tail && (lane == 31 || !next_takes);
     if (tail_out) atomic_add_frag(a.C + int64_t(last_row) * a.ldc + col0, tail);
 }

@@ -45,7 +45,7 @@ static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cud
     switch (p.V) {
         case 1: k_eb_sr_thr<float, false, 1, 15><<<p.grid, kThreads, 0, s>>>(a); break;
         case 2: k_eb_sr_thr<float, false, 2, 15><<<p.grid, kThreads, 0, s>>>(a); break;
-        case 4: k_eb_sr_thr<float, false, 4, 8><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 4: k_eb_sr_thr<float, false, 4, 7><<<p.grid, kThreads, 0, s>>>(a); break;
         default: return cudaErrorNotSupported;
     }
     return cudaGetLastError();
