@@ -111,6 +111,15 @@ static int64_t max_tile_cols(const daspmm_csr* h, int64_t N) {
     return 256;
 }
 
+// DASPMM_EB_CTA=0 disables the CTA-combined EB+SR path (tuning aid).
+static bool eb_cta_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("DASPMM_EB_CTA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // EB chunk count for a chunk length; DASPMM_EB_CHUNK overrides the length (tuning aid).
 static int64_t auto_chunks(int64_t nnz, int64_t chunk) {
     if (nnz <= 0) return 1;
@@ -172,7 +181,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             p.sub = p.V >= 4 ? 7 : 15;  // odd; 3 x sub x 256 x 4 B of staging < 48 KB
             p.P = (h->nnz + p.sub - 1) / p.sub;
             workers = p.P;
-        } else if (!pr && !exact && P <= 0) {  // fast path: CTA-combined boundary rows
+        } else if (!pr && !exact && P <= 0 && eb_cta_enabled()) {  // CTA-combined boundary rows
             p.cta = true;
             p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
             p.sub = std::max<int64_t>(p.sub, 1);
@@ -228,6 +237,8 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     a.rpg = p.rpg;
     a.sub = p.sub;
     a.rows = h->coo_rows;
+    a.bulk_ok = (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->va) |
+                   reinterpret_cast<uintptr_t>(h->coo_rows)) & 15) == 0) ? 1 : 0;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if (eb) {
         cudaError_t e =

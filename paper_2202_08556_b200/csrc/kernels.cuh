@@ -39,6 +39,7 @@ struct SpmmArgs {
     int seg;                     // exact-mode EB+SR staging segment, max(W, 256)
     int64_t rpg;                 // RB: rows per group (row-block size)
     int64_t sub;                 // EB fast path: pairs per group sub-chunk
+    int bulk_ok;                 // A arrays 16-B aligned: CTA tiles may be staged by TMA
     const int* __restrict__ chunk_row;  // EB: row holding each chunk's first element
     const int* __restrict__ rows;       // EB: COO row id of every nonzero (handle-owned)
 };
@@ -360,13 +361,28 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
 template <typename T, bool CM, int V, int S>
 __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) {
     static_assert(S % 2 == 1, "odd S keeps the per-thread strided reads conflict-free");
-    constexpr int PITCH = 1;  // natural order: pair i of thread t at [t*S + i]
-    __shared__ int s_c[S * kThreads];
-    __shared__ int s_r[S * kThreads];
-    __shared__ T s_v[S * kThreads];
+    static_assert((kThreads * S * sizeof(int)) % 16 == 0, "TMA bulk size granularity");
+    // natural order: pair i of thread t at [t*S + i]
+    __shared__ __align__(16) int s_c[S * kThreads];
+    __shared__ __align__(16) int s_r[S * kThreads];
+    __shared__ __align__(16) T s_v[S * kThreads];
+    __shared__ uint64_t bar;
     const int64_t E0 = int64_t(blockIdx.x) * kThreads * S;
     const int64_t E1 = min(a.nnz, E0 + int64_t(kThreads) * S);
-    {  // coalesced staging; every load of the tile is issued before any store
+    if (a.bulk_ok && E1 - E0 == int64_t(kThreads) * S) {
+        // Full tile: three 1-D TMA bulk copies, one elected thread, mbarrier completion.
+        constexpr unsigned kIdxBytes = kThreads * S * sizeof(int);
+        constexpr unsigned kValBytes = kThreads * S * sizeof(T);
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(&bar, 2 * kIdxBytes + kValBytes);
+            bulk_g2s(s_c, a.ci + E0, kIdxBytes, &bar);
+            bulk_g2s(s_v, a.va + E0, kValBytes, &bar);
+            bulk_g2s(s_r, a.rows + E0, kIdxBytes, &bar);
+        }
+        mbar_wait(&bar, 0);
+    } else {  // ragged tail tile: coalesced loads, all issued before any store
         int lc[S], lr[S];
         T lv[S];
 #pragma unroll
@@ -384,8 +400,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
             s_v[jj] = lv[k];
             s_r[jj] = lr[k];
         }
+        __syncthreads();
     }
-    __syncthreads();
     const int t = threadIdx.x;
     const int lane = t & 31;
     const int64_t e0 = E0 + int64_t(t) * S;
