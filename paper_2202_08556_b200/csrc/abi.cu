@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -131,6 +132,63 @@ static int64_t auto_chunks(int64_t nnz, int64_t chunk) {
     return (nnz + chunk - 1) / chunk;
 }
 
+// DASPMM_LEAN=0 disables the lean SR kernels; DASPMM_LEAN_MIN_LANES (default 4) is the
+// narrowest lane group they take; DASPMM_LEAN_CHUNK the EB chunk (tuning aids).
+static bool lean_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("DASPMM_LEAN");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+static int lean_min_lanes() {
+    static const int v = [] {
+        const char* e = getenv("DASPMM_LEAN_MIN_LANES");
+        return e ? atoi(e) : 4;
+    }();
+    return v;
+}
+static int64_t lean_chunk(int lanes) {
+    static const int64_t env = [] {
+        const char* e = getenv("DASPMM_LEAN_CHUNK");
+        return e ? int64_t(atoll(e)) : int64_t(0);
+    }();
+    (void)lanes;
+    return env > 0 ? env : 128;
+}
+
+// DASPMM_WIN=1 enables the RB+SR B-window kernel (opt-in: on B200 the L1 already
+// serves row-local gathers, measured no gain; kept as a tuning aid).
+static bool win_enabled() {  // read per plan so tests can toggle it
+    const char* e = getenv("DASPMM_WIN");
+    return e && e[0] == '1';
+}
+
+// RB+RM+SR on row-local matrices: stage each CTA panel's B window in shared memory
+// (k_rb_sr_win) when the windows are narrow enough to fit and every staged B row is
+// reused by several nonzeros. The panel height is the largest R = 32 << i that still
+// gives >= 2 CTAs per SM; the staging must fit kWinSmemMax for the widest panel.
+static void plan_window(const daspmm_csr* h, Plan& p, int64_t N, int64_t tile_cols,
+                        int64_t ytiles, const void* B, bool exact) {
+    p.win_rows = 0;
+    if (exact || p.cm || h->dtype != DASPMM_F32 || !win_enabled() || h->spans == nullptr ||
+        h->M <= 0 || h->nnz <= 0 || B == nullptr)
+        return;
+    const int64_t pitch = std::min<int64_t>(N, tile_cols);
+    const int64_t row_bytes = pitch * 4;
+    const double avg = double(h->nnz) / double(h->M);
+    for (int i = daspmm_csr::kSpanLevels - 1; i >= 0; --i) {
+        const int64_t R = int64_t(32) << i;
+        if ((h->M + R - 1) / R * ytiles < 2 * 148 && i > 0) continue;
+        const int64_t smem = h->span_max[i] * row_bytes + 16;
+        if (size_t(smem) > kWinSmemMax) continue;
+        if (h->span_avg[i] <= 0 || avg * double(R) / h->span_avg[i] < 3.0) return;
+        p.win_rows = int(R);
+        p.win_smem = size_t(smem);
+        return;
+    }
+}
+
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
                int64_t ldb, const void* C, int64_t ldc, bool exact) {
     Plan p;
@@ -166,9 +224,38 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         tile_cols = int64_t(p.L) * p.X * p.V;
         lanes = p.L;
     }
+    // Lean SR kernels (lean.cuh): fp32 fast mode, row-major B, groups of >= 2 lanes,
+    // quad-aligned A arrays. One column slot per lane; wider N takes more y-tiles.
+    p.lean = !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 && lean_enabled() &&
+             p.L >= lean_min_lanes() && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
+             (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
+                                           reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
+    // Row-local matrices (narrow column windows, e.g. banded) keep k_rb_sr from N = 32
+    // on: its shuffle-broadcast walk reuses L1-resident B rows better (measured: banded
+    // s20 N = 32 188 vs 211 us, N = 128 582 vs 606 us).
+    if (p.lean && !eb && N >= 32 && h->span_avg[0] > 0 &&
+        h->span_avg[0] < 8.0 * double(h->nnz) / double(std::max<int64_t>(h->M, 1)))
+        p.lean = false;
+    if (p.lean) {
+        p.X = 1;
+        tile_cols = int64_t(p.L) * p.V;
+    }
     const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
     int64_t workers;
-    if (eb) {
+    if (eb && p.lean) {
+        // short rows: range walk (COO ids per block); long rows: segment walk.
+        // DASPMM_LEAN_RW=0/1 forces one (tuning aid).
+        const char* rw = getenv("DASPMM_LEAN_RW");
+        const double avg_nonempty = h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty)
+                                                      : 0.0;
+        // Measured on B200 (profiles/r01_notes.md §lean): range walk wins on power-law
+        // rows up to N = 64 (s20: 342 -> 217 us at N = 16), the segment walk on long rows
+        // (c3: 5.26 -> 4.07 ms) and at N = 128.
+        p.lean_rw = rw ? rw[0] == '1' : (avg_nonempty < 48.0 && N <= 64);
+        p.sub = lean_chunk(p.L);
+        p.P = (h->nnz + p.sub - 1) / p.sub;
+        workers = std::max<int64_t>(p.P, 1);
+    } else if (eb) {
         // Measured on B200 (profiles/r01_notes.md): short chunks win — 32 pairs per
         // group (64 for full-warp SR groups), the split-row atomics are cheap.
         const int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
@@ -204,8 +291,21 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             return e ? int64_t(atoll(e)) : int64_t(0);
         }();
         if (env_rpg > 0) rpg = std::min<int64_t>(env_rpg, p.L);
+        if (p.lean) {
+            static const int64_t env_lrpg = [] {
+                const char* e = getenv("DASPMM_LEAN_RPG");
+                return e ? int64_t(atoll(e)) : int64_t(0);
+            }();
+            if (env_lrpg > 0) rpg = env_lrpg;
+        }
         p.rpg = rpg;
         workers = (h->M + rpg - 1) / rpg;
+        plan_window(h, p, N, tile_cols, ytiles, B, exact);
+        if (p.win_rows > 0) {
+            p.lean = false;
+            p.grid = dim3(unsigned((h->M + p.win_rows - 1) / p.win_rows), unsigned(ytiles), 1);
+            return p;
+        }
     } else {
         workers = h->M;
     }
@@ -237,9 +337,22 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     a.rpg = p.rpg;
     a.sub = p.sub;
     a.rows = h->coo_rows;
+    a.spans = h->spans;
+    a.win_rows = p.win_rows;
     a.bulk_ok = (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->va) |
                    reinterpret_cast<uintptr_t>(h->coo_rows)) & 15) == 0) ? 1 : 0;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
+    if constexpr (std::is_same<T, float>::value) {
+        if (p.lean) {
+            if (eb) {  // prologue: split rows at chunk ends and empty rows are zeroed
+                cudaError_t e = launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, 1,
+                                                          static_cast<T*>(C), ldc, int(N),
+                                                          h->empty_rows, int(h->n_empty), s);
+                if (e != cudaSuccess) return e;
+            }
+            return launch_sr_lean(p, a, s);
+        }
+    }
     if (eb) {
         cudaError_t e =
             (p.cta || p.thr)
@@ -265,12 +378,15 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     if (h->M == 0 || N == 0) return DASPMM_OK;
     if (chunk_scratch == nullptr) keep_pool_warm(h->device);  // never inside a graph capture
     const bool exact = (flags & DASPMM_EXACT) != 0;
+    const bool own_scratch = chunk_scratch == nullptr;
+    // EB kernels and the lean SR kernels read COO row ids (graph bodies get the array
+    // built before capture).
+    if (own_scratch && (kernel >= 4 || !(kernel & 1)))
+        if (int rc = ensure_coo(h, s)) return rc;
     const Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
     int* chunk_row = chunk_scratch;
-    const bool own_scratch = chunk_scratch == nullptr;
     cudaError_t e;
-    if (kernel >= 4 && own_scratch) {  // (graph bodies get the COO array built beforehand)
-        if (int rc = ensure_coo(h, s)) return rc;
+    if (kernel >= 4 && own_scratch) {
         if ((e = cudaMallocAsync(&chunk_row, sizeof(int) * size_t(std::max<int64_t>(p.P, 1)), s)) !=
             cudaSuccess)
             return cuda_fail(e, "cudaMallocAsync(chunk_row)");
@@ -543,6 +659,7 @@ int daspmm_csr_destroy(daspmm_csr* h) {
     cudaFree(h->empty_rows);
     cudaFree(h->d_feat);
     cudaFree(h->coo_rows);
+    cudaFree(h->spans);
     delete h;
     return DASPMM_OK;
 }
@@ -679,6 +796,18 @@ int daspmm_partition(const daspmm_csr* h, int64_t p, int64_t* begin, int64_t* en
         if (row) row[i] = rows[size_t(i)];
         start += size;
     }
+    return DASPMM_OK;
+}
+
+int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, int64_t ldb,
+                     const void* C, int64_t ldc, unsigned flags, int* variant, int64_t* param) {
+    if (!h || !variant || !param) return fail(DASPMM_ERR_INVALID_ARG, "plan_info: null argument");
+    if (kernel < 0 || kernel > 7) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
+    if (int rc = ensure_coo(h, 0)) return rc;
+    const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
+    *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : 0;
+    *param = p.win_rows > 0 ? p.win_rows : (p.thr || (p.lean && kernel >= 4)) ? p.sub
+             : p.lean ? p.rpg : 0;
     return DASPMM_OK;
 }
 

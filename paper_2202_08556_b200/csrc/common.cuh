@@ -72,6 +72,30 @@ __device__ __forceinline__ Frag<T, V> ld_frag(const T* __restrict__ p) {
     return f;
 }
 
+// V consecutive elements from shared memory (the staged B window). Plain C++ loads: the
+// pointer derives from the kernel's shared array, so ptxas emits LDS (checked in SASS).
+template <typename T, int V>
+__device__ __forceinline__ Frag<T, V> ld_frag_shared(const T* p) {
+    Frag<T, V> f;
+    if constexpr (V == 1) {
+        f.v[0] = *p;
+    } else {
+        using VT = typename VecT<T, V>::type;
+        *reinterpret_cast<VT*>(f.v) = *reinterpret_cast<const VT*>(p);
+    }
+    return f;
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void st_frag_shared(T* p, const Frag<T, V>& f) {
+    if constexpr (V == 1) {
+        *p = f.v[0];
+    } else {
+        using VT = typename VecT<T, V>::type;
+        *reinterpret_cast<VT*>(p) = *reinterpret_cast<const VT*>(f.v);
+    }
+}
+
 // Column-major B: V columns at stride ldb, scalar loads.
 template <typename T, int V>
 __device__ __forceinline__ Frag<T, V> ld_frag_cm(const T* __restrict__ p, int64_t ldb) {

@@ -23,9 +23,18 @@ struct Plan {
     bool cta = false;    // EB+SR fast path: CTA-combined boundary rows (k_eb_sr_cta)
     bool thr = false;    // EB+SR fast path for one-lane groups: staged sub-chunks (k_eb_sr_thr)
     int64_t sub = 0;     // ... its pairs per group sub-chunk
+    bool lean = false;   // RB/EB+RM+SR lean kernels (lean.cuh), fp32 fast mode
+    bool lean_rw = false;  // ... EB: range walk with COO row ids (short rows)
+    int win_rows = 0;    // RB+SR window kernel (k_rb_sr_win): rows per CTA panel, 0 = off
+    size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
 };
 
+// Largest dynamic shared memory of the RB window kernel (B window + alignment lead);
+// three CTAs per SM fit in the 228 KB carveout.
+constexpr size_t kWinSmemMax = 72 * 1024;
+
 // Each returns cudaErrorNotSupported for a shape with no instantiation.
+cudaError_t launch_sr_lean(const Plan&, const SpmmArgs<float>&, cudaStream_t);
 template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);

@@ -9,7 +9,10 @@
 // interval [std_lo, std_hi] around the parallel sum. A tree threshold outside that
 // interval is decided exactly; one inside it (never seen in practice) triggers the
 // sequential replay kernel below, which reproduces the reference bits.
+#include <algorithm>
+#include <climits>
 #include <cmath>
+#include <vector>
 
 #include "internal.h"
 
@@ -98,6 +101,63 @@ int ensure_coo(const daspmm_csr* hc, cudaStream_t s) {
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "coo_rows");
 }
 
+// Column window of every 32-row fine panel: one warp per panel, [min, max] column
+// ({INT_MAX, -1} when the panel holds no nonzero).
+__global__ void k_fine_spans(const int* __restrict__ rp, const int* __restrict__ ci, int M,
+                             int64_t n_fine, int2* __restrict__ spans) {
+    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n_fine) return;
+    const int r0 = int(p * 32), r1 = min(M, r0 + 32);
+    const int s = __ldg(rp + r0), e = __ldg(rp + r1);
+    int lo = INT_MAX, hi = -1;
+    for (int i = s + lane; i < e; i += 32) {
+        const int c = __ldg(ci + i);
+        lo = min(lo, c);
+        hi = max(hi, c);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) spans[p] = make_int2(lo, hi);
+}
+
+// Fine-panel windows on the device plus, per panel height R = 32 << i, the widest and
+// the mean window (host), which plan_spmm uses to size the window kernel's staging.
+static int compute_spans(daspmm_csr* h, cudaStream_t s) {
+    h->n_fine = (h->M + 31) / 32;
+    if (h->n_fine == 0) return DASPMM_OK;
+    cudaError_t e = cudaMalloc(&h->spans, sizeof(int2) * size_t(h->n_fine));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(spans)");
+    const int64_t threads = h->n_fine * 32;
+    k_fine_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M),
+                                                                 h->n_fine, h->spans);
+    std::vector<int2> hs(size_t(h->n_fine));
+    cudaMemcpyAsync(hs.data(), h->spans, sizeof(int2) * hs.size(), cudaMemcpyDeviceToHost, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "spans");
+    for (int i = 0; i < daspmm_csr::kSpanLevels; ++i) {
+        const int64_t k = int64_t(1) << i;
+        int64_t mx = 0, cnt = 0;
+        double sum = 0.0;
+        for (int64_t p = 0; p < h->n_fine; p += k) {
+            int lo = INT_MAX, hi = -1;
+            for (int64_t q = p; q < std::min(h->n_fine, p + k); ++q) {
+                lo = std::min(lo, hs[q].x);
+                hi = std::max(hi, hs[q].y);
+            }
+            if (hi < lo) continue;
+            const int64_t w = int64_t(hi) - lo + 1;
+            mx = std::max(mx, w);
+            sum += double(w);
+            ++cnt;
+        }
+        h->span_max[i] = mx;
+        h->span_avg[i] = cnt ? sum / double(cnt) : 0.0;
+    }
+    return DASPMM_OK;
+}
+
 int compute_features(daspmm_csr* h, cudaStream_t s) {
     const int M = int(h->M);
     DevFeatures f{};
@@ -168,7 +228,7 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
                              s)) != cudaSuccess)
         return cuda_fail(e, "cudaMemcpy(features)");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
-    return DASPMM_OK;
+    return compute_spans(h, s);
 }
 
 int exact_std(daspmm_csr* h, double* out) {

@@ -60,6 +60,13 @@ struct daspmm_csr {
     std::mutex mu;                          // guards the lazy exact-std cache
     void* graph_cache = nullptr;            // graph.cu
     int32_t* coo_rows = nullptr;            // EB kernels: row id per nonzero (built lazily)
+    // Column windows (RB+SR window kernel): [min col, max col] of every 32-row fine panel
+    // (device), and for panels of R = 32 << i rows the largest and mean window width.
+    int2* spans = nullptr;
+    int64_t n_fine = 0;
+    static constexpr int kSpanLevels = 8;
+    int64_t span_max[kSpanLevels] = {};
+    double span_avg[kSpanLevels] = {};
 };
 
 namespace daspmm {

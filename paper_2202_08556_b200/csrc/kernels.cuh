@@ -42,6 +42,8 @@ struct SpmmArgs {
     int bulk_ok;                 // A arrays 16-B aligned: CTA tiles may be staged by TMA
     const int* __restrict__ chunk_row;  // EB: row holding each chunk's first element
     const int* __restrict__ rows;       // EB: COO row id of every nonzero (handle-owned)
+    const int2* __restrict__ spans;     // RB window kernel: column window per 32-row panel
+    int win_rows;                       // RB window kernel: rows per CTA panel (32 << i)
 };
 
 constexpr int kThreads = 256;
@@ -80,13 +82,24 @@ struct CtaSlots {
     int tn = 0;          // tile width
 };
 
-enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2 };
+enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2, kRBWin = 3 };
+
+// RB window kernel: the CTA's B rows [c0, c0 + span) staged in shared memory, `pitch`
+// elements per row starting at column tile0.
+template <typename T>
+struct WinSlots {
+    const T* s = nullptr;
+    int c0 = 0;
+    int pitch = 0;
+    int tile0 = 0;
+};
 
 template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE>
 __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, const int e1, int r,
                                         const int nrows, const int n0, const unsigned mask,
-                                        const int gl, const CtaSlots<T> slots = CtaSlots<T>{}) {
-    constexpr bool EB = MODE != kRB;
+                                        const int gl, const CtaSlots<T> slots = CtaSlots<T>{},
+                                        const WinSlots<T> win = WinSlots<T>{}) {
+    constexpr bool EB = MODE == kEB || MODE == kEBCta;
     constexpr int STEP = LPR >= 16 ? LPR : (LPR >= 4 ? 16 : 8);  // pairs per group per step
     constexpr int EPL = STEP / LPR;                              // pairs per lane per step
     // Double-buffered A pairs pay off once a lane holds few of them (LPR >= 4); narrow
@@ -188,7 +201,14 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 #pragma unroll
                     for (int s = 0; s < CPL; ++s) {
                         const int col = n0 + s * LPR * V;
-                        if (col < a.N) b[u][s] = gather<T, CM, V>(a, u < nb ? ct : 0, col);
+                        if constexpr (MODE == kRBWin) {
+                            const int k = u < nb ? ct - win.c0 : 0;
+                            if (col < a.N)
+                                b[u][s] = ld_frag_shared<T, V>(win.s + int64_t(k) * win.pitch +
+                                                               (col - win.tile0));
+                        } else {
+                            if (col < a.N) b[u][s] = gather<T, CM, V>(a, u < nb ? ct : 0, col);
+                        }
                     }
                 }
                 const int ef = j + x0;
@@ -273,6 +293,88 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     const int n0 = blockIdx.y * TN + gl * V;
     sr_walk<T, CM, EXACT, V, LPR, CPL, kRB>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0),
                                             r1 - int(r0), n0, mask, gl);
+}
+
+// RB + SR with the B window in shared memory (row-local matrices: banded, meshes).
+// A CTA owns a panel of win_rows rows. The union of the panel's column indices is a
+// window [c0, c1] (precomputed per 32-row fine panel at handle creation); the CTA stages
+// B rows c0..c1 of its column tile into shared memory once — one 1-D TMA bulk copy when
+// the rows are contiguous (whole-row tile, ldb == N), cooperative vector loads otherwise
+// — and every gather of the walk is a shared-memory load. B then crosses L2 about once
+// per panel instead of once per nonzero, so the call streams at HBM rate.
+// Groups take the panel's row blocks round-robin; rows, order and arithmetic are those
+// of k_rb_sr (spmm.hpp:66-88).
+template <typename T, int V, int LPR, int CPL>
+__global__ void __launch_bounds__(kThreads, 3) k_rb_sr_win(const SpmmArgs<T> a, int bulk_b) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ uint64_t bar;
+    __shared__ int s_win[2];
+    constexpr int TN = LPR * V * CPL;
+    constexpr int G = kThreads / LPR;
+    const int64_t R0 = int64_t(blockIdx.x) * a.win_rows;
+    const int r_end = int(min(int64_t(a.M), R0 + a.win_rows));
+    if (threadIdx.x < 32) {  // the panel's window from its fine panels
+        const int64_t f0 = R0 / 32, f1 = (int64_t(r_end) + 31) / 32;
+        int lo = INT_MAX, hi = -1;
+        for (int64_t f = f0 + threadIdx.x; f < f1; f += 32) {
+            const int2 w = __ldg(a.spans + f);
+            lo = min(lo, w.x);
+            hi = max(hi, w.y);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(kFull, lo, o));
+            hi = max(hi, __shfl_xor_sync(kFull, hi, o));
+        }
+        if (threadIdx.x == 0) {
+            s_win[0] = lo;
+            s_win[1] = hi;
+            mbar_init(&bar, 1);
+        }
+    }
+    __syncthreads();
+    const int c0 = s_win[0], c1 = s_win[1];
+    const int tile0 = blockIdx.y * TN;
+    const int pitch = min(a.N - tile0, TN);
+    T* sB = reinterpret_cast<T*>(dsm);
+    if (c1 >= c0) {
+        const int64_t span = int64_t(c1) - c0 + 1;
+        if (bulk_b && gridDim.y == 1 && pitch == a.N && a.ldb == a.N) {
+            // contiguous rows: one bulk copy from the 16-B aligned address below B[c0]
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.B + int64_t(c0) * a.N);
+            const unsigned lead = unsigned(reinterpret_cast<uintptr_t>(src) & 15u);
+            const unsigned char* src_al = src - lead;
+            const unsigned total = lead + unsigned(span * a.N * int64_t(sizeof(T)));
+            const unsigned bulk = total & ~15u;
+            sB = reinterpret_cast<T*>(dsm + lead);
+            if (threadIdx.x == 0 && bulk > 0) {
+                mbar_expect_tx(&bar, bulk);
+                bulk_g2s(dsm, src_al, bulk, &bar);
+            }
+            for (unsigned i = bulk + threadIdx.x; i < total; i += kThreads) dsm[i] = __ldg(src_al + i);
+            if (bulk > 0) mbar_wait(&bar, 0);
+        } else {
+            const int nvec = pitch / V;
+            for (int64_t i = threadIdx.x; i < span * nvec; i += kThreads) {
+                const int64_t row = i / nvec;
+                const int j = int(i - row * nvec);
+                st_frag_shared<T, V>(sB + row * pitch + j * V,
+                                     ld_frag<T, V>(a.B + (c0 + row) * a.ldb + tile0 + j * V));
+            }
+        }
+    }
+    __syncthreads();
+    const WinSlots<T> win{sB, c0, pitch, tile0};
+    const unsigned mask = group_mask<LPR>();
+    const int gl = threadIdx.x & (LPR - 1);
+    const int g = threadIdx.x / LPR;
+    const int n0 = tile0 + gl * V;
+    const int nblk = int((r_end - R0 + a.rpg - 1) / a.rpg);
+    for (int blk = g; blk < nblk; blk += G) {
+        const int r0 = int(R0) + blk * int(a.rpg);
+        const int r1 = min(r_end, r0 + int(a.rpg));
+        sr_walk<T, false, false, V, LPR, CPL, kRBWin>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), r0,
+                                                      r1 - r0, n0, mask, gl, CtaSlots<T>{}, win);
+    }
 }
 
 // EB + SR: group w owns partition chunk w (partition.hpp:45-64).

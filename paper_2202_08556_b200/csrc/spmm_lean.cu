@@ -1,0 +1,36 @@
+// Launchers of the lean SR kernels (lean.cuh): RB+RM+SR and EB+RM+SR, fp32 fast mode.
+#include "dispatch.h"
+#include "lean.cuh"
+
+namespace daspmm {
+
+#define DASPMM_LEAN_LPR(KERN, V)                                                      \
+    switch (p.L) {                                                                   \
+        case 2: KERN<V, 2><<<p.grid, kThreads, 0, s>>>(a); break;                    \
+        case 4: KERN<V, 4><<<p.grid, kThreads, 0, s>>>(a); break;                    \
+        case 8: KERN<V, 8><<<p.grid, kThreads, 0, s>>>(a); break;                    \
+        case 16: KERN<V, 16><<<p.grid, kThreads, 0, s>>>(a); break;                  \
+        case 32: KERN<V, 32><<<p.grid, kThreads, 0, s>>>(a); break;                  \
+        default: return cudaErrorNotSupported;                                       \
+    }
+
+#define DASPMM_LEAN_V(KERN)                                                           \
+    switch (p.V) {                                                                   \
+        case 1: { DASPMM_LEAN_LPR(KERN, 1) } break;                                  \
+        case 2: { DASPMM_LEAN_LPR(KERN, 2) } break;                                  \
+        case 4: { DASPMM_LEAN_LPR(KERN, 4) } break;                                  \
+        default: return cudaErrorNotSupported;                                       \
+    }
+
+cudaError_t launch_sr_lean(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.kernel >= 4 && p.lean_rw) {
+        DASPMM_LEAN_V(k_eb_sr_lean_rw)
+    } else if (p.kernel >= 4) {
+        DASPMM_LEAN_V(k_eb_sr_lean)
+    } else {
+        DASPMM_LEAN_V(k_rb_sr_lean)
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace daspmm

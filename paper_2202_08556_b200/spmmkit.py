@@ -379,6 +379,20 @@ def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int 
     return C_out
 
 
+PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean"}
+
+
+def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False):
+    """(variant name, parameter) of the launch daspmm_spmm would run for these
+    row-major device operands — diagnostics (see daspmm_plan_info)."""
+    kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
+    v, prm = C.c_int(), C.c_int64()
+    check(lib().daspmm_plan_info(a._h, kid, B.shape[1], B.data_ptr(), _ld(B), C_out.data_ptr(),
+                                 _ld(C_out), _lib.EXACT if exact else 0, C.byref(v),
+                                 C.byref(prm)))
+    return PLAN_VARIANTS[v.value], prm.value
+
+
 # ------------------------------------------------------------------ features / partition
 @dataclass
 class FeatureVector:

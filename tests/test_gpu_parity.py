@@ -405,3 +405,110 @@ def test_auto_layout_tall_operand(sk):
     torch.cuda.synchronize()
     y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
     assert (np.abs(Cc.cpu().numpy() - y64) <= H.gamma_bound(a, x, np.float32)).all()
+
+
+def _banded_csr(M, b, seed, empty_every=0):
+    """Banded CSR (row r holds columns [r-b, r+b] ∩ [0, M)); every empty_every-th
+    row left empty, plus one fully empty 64-row block."""
+    from paper_2202_08556_b200.spmmkit import CsrMatrix
+
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for r in range(M):
+        if (empty_every and r % empty_every == 0) or 1000 <= r < 1064:
+            continue
+        c = np.arange(max(0, r - b), min(M, r + b + 1))
+        rows.append(np.full(c.size, r))
+        cols.append(c)
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    rp = np.zeros(M + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    va = rng.uniform(-1, 1, cols.size).astype(np.float32)
+    return CsrMatrix(M, M, rp, cols.astype(np.int64), va, np.float32)
+
+
+@pytest.mark.parametrize("b", [2, 8, 30])
+def test_rb_window_kernel_banded(sk, b):
+    """RB+RM+SR on row-local matrices runs k_rb_sr_win (B window staged in shared
+    memory, TMA bulk copy when rows are contiguous). Contiguous B, padded ldb and a
+    B pointer off the 16-byte grid (TMA lead bytes) all stay within the gamma bound."""
+    import torch
+
+    import os
+
+    a = _banded_csr(6000, b, seed=b, empty_every=7)
+    d = sk.DeviceCsr.from_host(a)
+    os.environ["DASPMM_WIN"] = "1"  # opt-in kernel (plan reads it per call)
+    bound_cache = {}
+    variants = set()
+    for n in (1, 2, 3, 4, 8, 16, 32, 33, 64, 100, 128, 256, 300):
+        x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
+        y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+        bound = bound_cache.setdefault(n, H.gamma_bound(a, x, np.float32))
+        for mode in ("contig", "padded", "offset"):
+            if mode == "contig":
+                B = torch.from_numpy(x).cuda()
+            elif mode == "padded":
+                B = torch.zeros(a.num_cols, n + 4, device="cuda")[:, :n]
+                B.copy_(torch.from_numpy(x))
+            else:  # one element past a 16-B boundary: the bulk copy needs lead bytes
+                buf = torch.zeros(a.num_cols * n + 1, device="cuda")
+                B = buf[1:].view(a.num_cols, n)
+                B.copy_(torch.from_numpy(x))
+            C = torch.full((a.num_rows, n), float("nan"), device="cuda")
+            variant, rows = sk.plan_info(0, d, B, C)
+            variants.add(variant)
+            sk.spmm_device(0, d, B, C)
+            torch.cuda.synchronize()
+            err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= bound).all(), f"b{b} n{n} {mode} ({variant}, {rows}): {err.max()}"
+    del os.environ["DASPMM_WIN"]
+    assert "rb_window" in variants
+
+
+def test_rb_window_not_used_on_scattered_columns(sk):
+    import os
+
+    import torch
+
+    a = H.random_csr(4000, 4000, 60000, seed=3, dtype=np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    B = torch.zeros(4000, 32, device="cuda")
+    C = torch.zeros(4000, 32, device="cuda")
+    os.environ["DASPMM_WIN"] = "1"
+    try:
+        assert sk.plan_info(0, d, B, C)[0] != "rb_window"
+    finally:
+        del os.environ["DASPMM_WIN"]
+
+
+@pytest.mark.parametrize("kernel", [0, 4])
+@pytest.mark.parametrize("skew", [0.0, 1.3])
+def test_lean_sr_kernels(sk, kernel, skew):
+    """Lean RB/EB+RM+SR kernels (quad-loaded A, one row segment per group): odd nnz
+    (scalar tail quad), empty rows, very long rows split over many EB chunks, N with
+    several y-tiles and padded ldb; within the gamma bound, every output written."""
+    import torch
+
+    a = H.random_csr(5003, 4001, 90001, seed=11 + kernel, dtype=np.float32, skew=skew)
+    d = sk.DeviceCsr.from_host(a)
+    seen = set()
+    for n in (8, 16, 24, 32, 64, 96, 128, 200, 256):
+        x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
+        y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+        bound = H.gamma_bound(a, x, np.float32)
+        for padded in (False, True):
+            if padded:
+                B = torch.zeros(a.num_cols, n + 8, device="cuda")[:, :n]
+                B.copy_(torch.from_numpy(x))
+            else:
+                B = torch.from_numpy(x).cuda()
+            C = torch.full((a.num_rows, n), float("nan"), device="cuda")
+            seen.add(sk.plan_info(kernel, d, B, C)[0])
+            sk.spmm_device(kernel, d, B, C)
+            torch.cuda.synchronize()
+            err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= bound).all(), f"k{kernel} n{n} padded={padded}: {np.nanmax(err)}"
+    assert "lean" in seen
