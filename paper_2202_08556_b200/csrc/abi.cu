@@ -132,7 +132,7 @@ static int64_t auto_chunks(int64_t nnz, int64_t chunk) {
     return (nnz + chunk - 1) / chunk;
 }
 
-// DASPMM_LEAN=0 disables the lean SR kernels; DASPMM_LEAN_MIN_LANES (default 4) is the
+// DASPMM_LEAN=0 disables the lean SR kernels; DASPMM_LEAN_MIN_LANES (default 2) is the
 // narrowest lane group they take; DASPMM_LEAN_CHUNK the EB chunk (tuning aids).
 static bool lean_enabled() {
     static const bool on = [] {
@@ -144,17 +144,17 @@ static bool lean_enabled() {
 static int lean_min_lanes() {
     static const int v = [] {
         const char* e = getenv("DASPMM_LEAN_MIN_LANES");
-        return e ? atoi(e) : 4;
+        return e ? atoi(e) : 2;
     }();
     return v;
 }
-static int64_t lean_chunk(int lanes) {
+static int64_t lean_chunk(bool range_walk) {
     static const int64_t env = [] {
         const char* e = getenv("DASPMM_LEAN_CHUNK");
         return e ? int64_t(atoll(e)) : int64_t(0);
     }();
-    (void)lanes;
-    return env > 0 ? env : 128;
+    // measured: 128 pairs for the range walk, 256 for the segment walk (c3 4.47 -> 4.34 ms)
+    return env > 0 ? env : (range_walk ? 128 : 256);
 }
 
 // DASPMM_WIN=1 enables the RB+SR B-window kernel (opt-in: on B200 the L1 already
@@ -252,7 +252,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // rows up to N = 64 (s20: 342 -> 217 us at N = 16), the segment walk on long rows
         // (c3: 5.26 -> 4.07 ms) and at N = 128.
         p.lean_rw = rw ? rw[0] == '1' : (avg_nonempty < 48.0 && N <= 64);
-        p.sub = lean_chunk(p.L);
+        p.sub = lean_chunk(p.lean_rw);
         p.P = (h->nnz + p.sub - 1) / p.sub;
         workers = std::max<int64_t>(p.P, 1);
     } else if (eb) {

@@ -33,6 +33,13 @@
 
 namespace daspmm {
 
+// Resident CTAs per SM the lean kernels are compiled for (register cap 65536 / (256 x
+// minB)). Measured on B200: the RB walk gains from 4 (64 registers, 32 warps: uniform
+// s20 N = 128 1294 -> 1245 us), the EB walks lose at 4 (power-law N = 16 range walk
+// 217 -> 303 us) and keep 3 (80 registers).
+constexpr int kLeanMinBlocksRB = 4;
+constexpr int kLeanMinBlocksEB = 3;
+
 struct Quad {
     int c[4];
     float v[4];
@@ -198,7 +205,7 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
 // RB: group g owns rows [g*rpg, (g+1)*rpg), one row segment at a time; every row is
 // owned (plain stores; empty rows store zeros).
 template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, 3) k_rb_sr_lean(const SpmmArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, kLeanMinBlocksRB) k_rb_sr_lean(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t g = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
     const int64_t r0 = g * a.rpg;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_rb_sr_lean(const SpmmArgs<float
 // segment at a time (next row from the COO id of the segment's end, so empty rows cost
 // nothing). Rows cut by the chunk ends take atomics. Suits long rows.
 template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, 3) k_eb_sr_lean(const SpmmArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, kLeanMinBlocksEB) k_eb_sr_lean(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_lean(const SpmmArgs<float
 // EB, range walk: the chunk as one nonzero range with COO row ids (range_walk). Suits
 // short rows (power-law tails), where per-segment row-offset lookups would dominate.
 template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, 3) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, kLeanMinBlocksEB) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
