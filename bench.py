@@ -305,15 +305,19 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                    "parallelism": f"row-panels x{world}, B replicated" if world > 1 else "1 GPU"},
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+        "roofline": {"bound": "hbm", "achieved": round(dom_ach, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(dom_ach / peak, 4), "traffic": traffic,
                      "peak_source": peak_kind,
-                     "scope": "suite aggregate: sum algorithmic bytes / sum call time",
+                     "scope": "dominant call (longest of the step): its algorithmic bytes "
+                              "(4(M+1)+8nnz+4N*K_touched+4NM) / its mean CUDA-event time",
                      "dominant": {"call": f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}',
                                   "kernel": sk.KernelId.from_index(chosen[dom]).name(),
                                   "ms": round(per_call_ms[dom], 4),
-                                  "achieved": round(dom_ach, 1),
-                                  "frac": round(dom_ach / peak, 4)}},
+                                  "algorithmic_bytes": calls[dom]["bytes"],
+                                  "ceilings_us": _ceilings(calls[dom], traffic, peak)},
+                     "suite_aggregate": {"achieved": round(achieved, 1),
+                                         "frac": round(achieved / peak, 4),
+                                         "scope": "sum algorithmic bytes / sum call time"}},
         "clocks": clk.summary(),
         "selected": {f'{c["m"]["name"]}/N{c["n"]}': sk.KernelId.from_index(k).name()
                      for c, k in zip(calls, chosen)},
@@ -331,6 +335,37 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _ceilings(c, traffic, peak):
+    """Lower bounds on one call's time (us), each from a measured B200 rate:
+    hbm        algorithmic bytes at the measured HBM copy bandwidth;
+    dram       ncu-measured DRAM bytes of the launch (profiles/, B re-reads included) at
+               the same bandwidth (null without a capture);
+    l2_gather  nnz B-row gathers (4N bytes each, whole 32-B sectors) at the measured random
+               L2->SM gather rate for that segment size (tools/gather_bw.cu,
+               profiles/gather_bw_r01.json; footprint <= 50 MB);
+    l1_wavefront  one L1 wavefront per (nonzero, 128-B line of its B row) at 1 per clock
+               per SM (148 SMs x 1.965 GHz) - the LSU floor for small N."""
+    import math
+
+    nnz, n = c["m"]["d"].nnz(), c["n"]
+    seg = max(32, 32 * math.ceil(4 * n / 32))
+    rate = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_bw_r01.json")) as fh:
+            g = json.load(fh)["gather"]
+        small = [x for x in g if x["footprint_mb"] <= 60]
+        best = [x for x in small if x["seg_bytes"] <= seg]
+        pick = max(best, key=lambda x: x["seg_bytes"]) if best else min(small, key=lambda x: x["seg_bytes"])
+        rate = pick["gbs"] * (seg / pick["seg_bytes"] if pick["seg_bytes"] < seg and pick["seg_bytes"] < 64 else 1.0)
+    except Exception:
+        pass
+    out = {"hbm": round(c["bytes"] / (peak * 1e9) * 1e6, 1),
+           "dram": round(traffic / (peak * 1e9) * 1e6, 1) if traffic else None,
+           "l2_gather": round(nnz * seg / (rate * 1e9) * 1e6, 1) if rate else None,
+           "l1_wavefront": round(nnz * math.ceil(4 * n / 128) / (148 * 1.965e9) * 1e6, 1)}
+    return out
 
 
 def _spot_check(c):

@@ -253,6 +253,10 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // (c3: 5.26 -> 4.07 ms) and at N = 128.
         p.lean_rw = rw ? rw[0] == '1' : (avg_nonempty < 48.0 && N <= 64);
         p.sub = lean_chunk(p.lean_rw);
+        // small matrices: shorten chunks until there are >= 4 CTAs per SM (s14 power-law,
+        // N = 128: 128 CTAs at 256 pairs -> 88 us, vs 32 us with the grid filled)
+        const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
+        if (!getenv("DASPMM_LEAN_CHUNK") && fill < p.sub) p.sub = std::max<int64_t>(32, fill & ~7LL);
         p.P = (h->nnz + p.sub - 1) / p.sub;
         workers = std::max<int64_t>(p.P, 1);
     } else if (eb) {
@@ -265,7 +269,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             h->dtype == DASPMM_F32) {
             // one-lane groups: CTA-staged thread sub-chunks (k_eb_sr_thr)
             p.thr = true;
-            p.sub = p.V >= 4 ? 7 : 15;  // odd; 3 x sub x 256 x 4 B of staging < 48 KB
+            p.sub = p.V >= 4 ? kThrS4 : kThrS;  // 3 x sub x 256 x 4 B of staging < 48 KB
             p.P = (h->nnz + p.sub - 1) / p.sub;
             workers = p.P;
         } else if (!pr && !exact && P <= 0 && eb_cta_enabled()) {  // CTA-combined boundary rows

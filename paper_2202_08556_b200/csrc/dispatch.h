@@ -29,6 +29,12 @@ struct Plan {
     size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
 };
 
+// Pairs per thread of the one-lane EB+SR path (k_eb_sr_thr). Measured on B200 (uniform
+// s20): V <= 2 takes 12 (4 x odd: 128-bit conflict-free shared reads; N = 2 129 -> 105
+// us), V = 4 keeps 7 (odd, scalar reads; 12 spent 80 registers and ran 126 -> 150 us).
+constexpr int kThrS = 12;
+constexpr int kThrS4 = 7;
+
 // Largest dynamic shared memory of the RB window kernel (B window + alignment lead);
 // three CTAs per SM fit in the 228 KB carveout.
 constexpr size_t kWinSmemMax = 72 * 1024;

@@ -462,7 +462,9 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
 // boundary take atomics (pre-zeroed by k_eb_prep_uniform with G = 1).
 template <typename T, bool CM, int V, int S>
 __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) {
-    static_assert(S % 2 == 1, "odd S keeps the per-thread strided reads conflict-free");
+    // Per-thread reads of the staged tile are conflict-free for odd S (scalar) and for
+    // S = 4 x odd (128-bit reads: 8 lanes per phase hit 8 distinct 16-B bank groups).
+    static_assert(S % 2 == 1 || (S % 4 == 0 && (S / 4) % 2 == 1), "conflict-free S");
     static_assert((kThreads * S * sizeof(int)) % 16 == 0, "TMA bulk size granularity");
     // natural order: pair i of thread t at [t*S + i]
     __shared__ __align__(16) int s_c[S * kThreads];
@@ -511,11 +513,36 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
     const bool active = e0 < e1;  // no early exit: the warp combines split rows below
     const int n = active ? int(e1 - e0) : 0;
     const int col0 = blockIdx.y * V;  // one V-wide column slot per thread
+    // this thread's pairs into registers (128-bit shared loads when S = 4k)
+    int cc[S], rr[S];
+    T vv[S];
+    if constexpr (S % 4 == 0 && sizeof(T) == 4) {
+#pragma unroll
+        for (int k = 0; k < S / 4; ++k) {
+            const int4 c4 = *reinterpret_cast<const int4*>(s_c + t * S + 4 * k);
+            const int4 r4 = *reinterpret_cast<const int4*>(s_r + t * S + 4 * k);
+            const float4 v4 = *reinterpret_cast<const float4*>(s_v + t * S + 4 * k);
+            cc[4 * k] = c4.x; cc[4 * k + 1] = c4.y; cc[4 * k + 2] = c4.z; cc[4 * k + 3] = c4.w;
+            rr[4 * k] = r4.x; rr[4 * k + 1] = r4.y; rr[4 * k + 2] = r4.z; rr[4 * k + 3] = r4.w;
+            vv[4 * k] = v4.x; vv[4 * k + 1] = v4.y; vv[4 * k + 2] = v4.z; vv[4 * k + 3] = v4.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            cc[i] = s_c[t * S + i];
+            rr[i] = s_r[t * S + i];
+            vv[i] = s_v[t * S + i];
+        }
+    }
     Frag<T, V> b[S];
 #pragma unroll
-    for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? s_c[t * S + i] : 0, col0);
-    const int first_row = active ? s_r[t * S] : INT_MAX;
-    const int last_row = active ? s_r[t * S + n - 1] : INT_MAX;
+    for (int i = 0; i < S; ++i) b[i] = gather<T, CM, V>(a, i < n ? cc[i] : 0, col0);
+    int last_row = rr[0];
+#pragma unroll
+    for (int i = 1; i < S; ++i)
+        if (i < n) last_row = rr[i];
+    const int first_row = active ? rr[0] : INT_MAX;
+    if (!active) last_row = INT_MAX;
     const int before = !active || e0 == 0 ? -1
                        : (t > 0 ? s_r[t * S - 1] : __ldg(a.rows + e0 - 1));
     const int after = !active || e1 >= a.nnz ? -1
@@ -541,12 +568,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
 #pragma unroll
     for (int i = 0; i < S; ++i) {
         if (i < n) {
-            const int rid = s_r[t * S + i];
+            const int rid = rr[i];
             if (rid != r) {
                 flush();
                 r = rid;
             }
-            const T v = s_v[t * S + i];
+            const T v = vv[i];
 #pragma unroll
             for (int q = 0; q < V; ++q) acc.v[q] = madd<false>(acc.v[q], v, b[i].v[q]);
         }
@@ -585,28 +612,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
     if (tail_out) atomic_add_frag(a.C + int64_t(last_row) * a.ldc + col0, tail);
 }
 
-// Prologue of the EB fast path: uniform sub-chunks of `sub` pairs; chunk_row for every
-// sub-chunk (row of its first pair, by binary search), split-row zeroing only at CTA
-// boundaries (every G-th sub-chunk), empty rows from the handle's list.
-template <typename T>
+// Prologue of the EB fast paths: zeroes the rows the EB kernel deposits into with
+// atomics — the row holding element k*G*sub when it continues from element k*G*sub - 1
+// (a split row at a CTA / chunk boundary) — and the empty rows (never visited by an EB
+// walker). One thread per (row, VZ-wide column vector): coalesced vector stores.
+template <typename T, int VZ>
 __global__ void __launch_bounds__(kThreads)
-k_eb_prep_uniform(const int* __restrict__ rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
+k_eb_prep_uniform(const int* __restrict__ rows, int64_t nnz, int64_t stride, int64_t n_bound,
                   T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty) {
-    const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (tid < n_sub) {
-        const int64_t b = tid * sub;
-        if (tid % G == 0 && b > 0 && b < nnz) {
-            const int row = __ldg(rows + b);
-            if (__ldg(rows + b - 1) == row) {
-                T* y = C + int64_t(row) * ldc;
-                for (int n = 0; n < N; ++n) y[n] = T(0);
-            }
-        }
-    } else if (tid - n_sub < int64_t(n_empty) * N) {
-        const int64_t k = tid - n_sub;
-        const int r = empty_rows[k / N];
-        C[int64_t(r) * ldc + k % N] = T(0);
+    const int nvec = (N + VZ - 1) / VZ;
+    const int64_t idx = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t item = idx / nvec;
+    const int j = int(idx - item * nvec);
+    int row;
+    if (item < n_bound) {
+        const int64_t b = (item + 1) * stride;  // boundary 0 never splits a row
+        if (b >= nnz) return;
+        row = __ldg(rows + b);
+        if (__ldg(rows + b - 1) != row) return;
+    } else if (item - n_bound < n_empty) {
+        row = __ldg(empty_rows + (item - n_bound));
+    } else {
+        return;
     }
+    Frag<T, VZ> z;
+#pragma unroll
+    for (int i = 0; i < VZ; ++i) z.v[i] = T(0);
+    st_frag_rw(C + int64_t(row) * ldc + int64_t(j) * VZ, z);
 }
 
 // =============================================================== RB + PR (K1 / K3)

@@ -43,9 +43,9 @@ DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
 
 static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
     switch (p.V) {
-        case 1: k_eb_sr_thr<float, false, 1, 15><<<p.grid, kThreads, 0, s>>>(a); break;
-        case 2: k_eb_sr_thr<float, false, 2, 15><<<p.grid, kThreads, 0, s>>>(a); break;
-        case 4: k_eb_sr_thr<float, false, 4, 7><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 1: k_eb_sr_thr<float, false, 1, kThrS><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 2: k_eb_sr_thr<float, false, 2, kThrS><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 4: k_eb_sr_thr<float, false, 4, kThrS4><<<p.grid, kThreads, 0, s>>>(a); break;
         default: return cudaErrorNotSupported;
     }
     return cudaGetLastError();
@@ -65,11 +65,20 @@ template <typename T>
 cudaError_t launch_eb_prep_uniform(const int* rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
                                    T* C, int64_t ldc, int N, const int* empty_rows, int n_empty,
                                    cudaStream_t s) {
-    const int64_t work = n_sub + int64_t(n_empty) * N;
+    const int64_t stride = sub * G;  // boundaries at stride, 2*stride, ... (< nnz)
+    const int64_t n_bound = n_sub > 0 ? (n_sub - 1) / G : 0;
+    const bool v4 = sizeof(T) == 4 && N % 4 == 0 && ldc % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+    const int vz = v4 ? 4 : 1;
+    const int64_t work = (n_bound + n_empty) * ((N + vz - 1) / vz);
     if (work == 0) return cudaSuccess;
-    const int64_t blocks = (work + kThreads - 1) / kThreads;
-    k_eb_prep_uniform<T><<<dim3(unsigned(blocks)), kThreads, 0, s>>>(
-        rows, nnz, sub, n_sub, G, C, ldc, N, empty_rows, n_empty);
+    const dim3 grid(unsigned((work + kThreads - 1) / kThreads));
+    if (v4)
+        k_eb_prep_uniform<T, (sizeof(T) == 4 ? 4 : 1)><<<grid, kThreads, 0, s>>>(
+            rows, nnz, stride, n_bound, C, ldc, N, empty_rows, n_empty);
+    else
+        k_eb_prep_uniform<T, 1><<<grid, kThreads, 0, s>>>(rows, nnz, stride, n_bound, C, ldc, N,
+                                                          empty_rows, n_empty);
     return cudaGetLastError();
 }
 template cudaError_t launch_eb_prep_uniform<float>(const int*, int64_t, int64_t, int64_t, int,
