@@ -106,6 +106,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _max_over_ranks(v: float, dev) -> float:
+    """Max of a per-rank scalar over all ranks (device tensor for NCCL, host for gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    on_dev = dist.get_backend() == "nccl"
+    tt = torch.tensor([v], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -126,16 +137,38 @@ def build_suite(small: bool, rank: int, world: int, workload: str = "suite"):
     for name, mk, ns in gen.workload(workload, small=small):
         M, K, rp, ci, va = mk()
         full = sk.DeviceCsr.from_device(M, K, rp, ci, va)
-        if world > 1:
-            cuts = multi.row_panel_cuts(rp.cpu().numpy(), world)
-            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-            d = full.panel(r0, r1)
-            torch.cuda.synchronize()
-        else:
-            r0, r1, d = 0, M, full
-        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), d=d, full=full,
-                         rows=(r0, r1), rp=rp, ci=ci, va=va, ns=ns))
+        mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), full=full,
+                         rp=rp, ci=ci, va=va, ns=ns))
     return mats
+
+
+def shard_calls(mats, ns_override, rank: int, world: int):
+    """This rank's share of the workload's (matrix, N) calls (multi.schedule_units):
+    large calls as nnz-balanced row panels (panel `rank` of each), the rest whole,
+    longest first to the least loaded rank. Returns [(matrix, N, handle, (r0, r1))]
+    and the list of every unit (for the whole-job flop count)."""
+    import torch
+
+    from paper_2202_08556_b200 import multi
+
+    units = [(m, n) for m in mats for n in (ns_override or m["ns"])]
+    costs = [multi.estimate_call_us(m["nnz_total"], n) for m, n in units]
+    assign, split = multi.schedule_units(costs, world)
+    panels = {}
+    mine = []
+    for i in assign[rank]:
+        m, n = units[i]
+        if split[i]:
+            if m["name"] not in panels:
+                cuts = multi.row_panel_cuts(m["rp"].cpu().numpy(), world)
+                r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+                panels[m["name"]] = (m["full"].panel(r0, r1), (r0, r1))
+                torch.cuda.synchronize()
+            d, rows = panels[m["name"]]
+        else:
+            d, rows = m["full"], (0, m["M"])
+        mine.append((m, n, d, rows))
+    return mine, units
 
 
 def run_ours(args):
@@ -145,11 +178,18 @@ def run_ours(args):
     from paper_2202_08556_b200 import spmmkit as sk
 
     world, rank, local = _dist()
+    # one process per GPU; ranks beyond the visible devices share them round-robin (only
+    # for exercising the multi-rank logic on a 1-GPU box with DASPMM_DIST_BACKEND=gloo)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("DASPMM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     sk.lib()  # fail loudly if the CUDA library is missing
     model = sk.load_selector(open(args.model).read())
@@ -158,21 +198,20 @@ def run_ours(args):
     ns_override = [int(n) for n in args.ns.split(",")] if args.ns else None
     ns = sorted({n for m in mats for n in (ns_override or m["ns"])})
 
-    # Operands per (matrix, N): B replicated, C local panel.
+    # Operands per (matrix, N) call of this rank: B replicated, C the local panel.
+    mine, units = shard_calls(mats, ns_override, rank, world)
     calls = []
-    for m in mats:
-        d = m["d"]
-        for n in (ns_override or m["ns"]):
-            B = gen.dense_operand(m["K"], n, seed=1000 + n, device=dev)
-            Cp = torch.empty(d.num_rows, n, device=dev)
-            kout = torch.zeros(1, dtype=torch.int32, device=dev)
-            calls.append(dict(m=m, n=n, B=B, C=Cp, kout=kout,
-                              flops=gen.flops(d.nnz(), n),
-                              bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), n, d.cols_touched)))
+    for m, n, d, rows in mine:
+        B = gen.dense_operand(m["K"], n, seed=1000 + n, device=dev)
+        Cp = torch.empty(d.num_rows, n, device=dev)
+        kout = torch.zeros(1, dtype=torch.int32, device=dev)
+        calls.append(dict(m=m, n=n, d=d, rows=rows, B=B, C=Cp, kout=kout,
+                          flops=gen.flops(d.nnz(), n),
+                          bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), n, d.cols_touched)))
     stream = torch.cuda.current_stream(dev)
 
     def one(c):
-        sk.spmm_selected(c["m"]["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream)
+        sk.spmm_selected(c["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream)
 
     def step(times=None):
         for i, c in enumerate(calls):
@@ -205,10 +244,8 @@ def run_ours(args):
     per_call_ms = [sum(s.elapsed_time(e) for s, e in t) / max(args.steps, 1) for t in times]
     step_ms = sum(per_call_ms)
     if world > 1:
-        tt = torch.tensor([step_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        step_ms = float(tt.item())
-    total_flops = sum(gen.flops(c["m"]["nnz_total"], c["n"]) for c in calls)
+        step_ms = _max_over_ranks(step_ms, dev)
+    total_flops = sum(gen.flops(m["nnz_total"], n) for m, n in units)  # all ranks' units
     value = total_flops / (step_ms * 1e-3) / 1e9
 
     # kernel choices and launch count: after the warm-up every call's decision is
@@ -272,9 +309,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
     torch.cuda.synchronize()
     e2e_ms = s.elapsed_time(e) / e2e_steps
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        e2e_ms = _max_over_ranks(e2e_ms, dev)
     e2e_value = total_flops / (e2e_ms * 1e-3) / 1e9
     return {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h}
@@ -302,7 +337,9 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                    "matrices": [m["name"] for m in mats], "ns": ns,
                    "calls_per_step": len(calls), "selector": os.path.basename(args.model),
                    "l2": "flushed (256 MiB write) before every timed call",
-                   "parallelism": f"row-panels x{world}, B replicated" if world > 1 else "1 GPU"},
+                   "parallelism": (f"{world} GPUs: calls sharded by multi.schedule_units (large calls "
+                                   "as nnz-balanced row panels, B replicated; the rest whole, LPT)")
+                                  if world > 1 else "1 GPU"},
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": round(dom_ach, 1), "peak": peak,
@@ -349,7 +386,7 @@ def _ceilings(c, traffic, peak):
                per SM (148 SMs x 1.965 GHz) - the LSU floor for small N."""
     import math
 
-    nnz, n = c["m"]["d"].nnz(), c["n"]
+    nnz, n = c["d"].nnz(), c["n"]
     seg = max(32, 32 * math.ceil(4 * n / 32))
     rate = None
     try:
@@ -375,7 +412,7 @@ def _spot_check(c):
     from oracle import oracle as O
 
     m = c["m"]
-    r0, r1 = m["rows"]
+    r0, r1 = c["rows"]
     rp = m["rp"].cpu().numpy().astype(np.int64)[r0:r1 + 1]
     rows = np.unique(np.linspace(0, r1 - r0 - 1, num=min(512, r1 - r0)).astype(np.int64))
     sub_rp = [0]
@@ -416,7 +453,7 @@ def _cusparse_compare(calls, flush, our_ms, ns):
     stream = torch.cuda.current_stream()
     best = []
     for c in calls:
-        d = c["m"]["d"]
+        d = c["d"]
         rp, ci, va = d.device_arrays()
         out = torch.empty_like(c["C"])
         ts = {}

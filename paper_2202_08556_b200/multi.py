@@ -11,6 +11,12 @@ Rows of C depend only on rows of A and columns of C only on the same columns of 
                              own panel's features.
   N-split (A replicated)     rank p owns columns [N*p/P, N*(p+1)/P) of B and C.
 
+A workload of many independent calls (the synthetic suite: 63 (matrix, N) calls) is
+sharded by `schedule_units`: calls too large for one rank's share are split into P row
+panels (panel p on rank p), the rest are assigned whole, longest first, to the least
+loaded rank (LPT). Every unit runs on exactly one rank; there is no collective on the
+data path.
+
 C stays sharded by default. `gather_rows` / `gather_cols` assemble it on every rank
 with NCCL all-gather when a consumer needs the full matrix (timed separately).
 """
@@ -41,6 +47,40 @@ def row_panel_cuts(row_offsets, parts: int) -> np.ndarray:
         r = row_of_element(rp, min(e, nnz - 1))
         cuts[p] = max(r, cuts[p - 1])
     return cuts
+
+
+def estimate_call_us(nnz: int, N: int, launch_us: float = 8.0) -> float:
+    """Rough B200 time of one DA-SpMM call for load balancing: a fixed launch cost plus
+    2 nnz N flops at ~3.5 TFLOP/s (the suite's measured average rate)."""
+    return launch_us + 2.0 * nnz * N / 3.5e6
+
+
+def schedule_units(costs, parts: int, split_frac: float = 0.5):
+    """Assign independent units (costs[i] = estimated time) to `parts` ranks.
+
+    A unit whose cost exceeds split_frac x the ideal per-rank load (sum / parts) is
+    split into `parts` row panels, panel p on rank p. The remaining units go whole,
+    largest first, to the rank with the least load so far (LPT).
+    Returns (assign, split): assign[r] = list of unit indices rank r runs (whole or its
+    panel); split[i] = True when unit i is row-split across all ranks."""
+    costs = [float(c) for c in costs]
+    parts = max(1, int(parts))
+    ideal = sum(costs) / parts
+    split = [parts > 1 and c > split_frac * ideal for c in costs]
+    load = [0.0] * parts
+    assign = [[] for _ in range(parts)]
+    for i, c in enumerate(costs):
+        if split[i]:
+            for r in range(parts):
+                assign[r].append(i)
+                load[r] += c / parts
+    for i in sorted((i for i in range(len(costs)) if not split[i]), key=lambda i: -costs[i]):
+        r = min(range(parts), key=lambda r: load[r])
+        assign[r].append(i)
+        load[r] += costs[i]
+    for r in range(parts):
+        assign[r].sort()
+    return assign, split
 
 
 def col_split(N: int, parts: int):

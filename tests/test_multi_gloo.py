@@ -110,3 +110,32 @@ def test_choose_partition_prefers_nsplit_for_wide_b():
     assert multi.choose_partition(1 << 25, 1 << 25, 503_316_480, 256, 8) == "cols"
     # narrow B, big A: row panels
     assert multi.choose_partition(1 << 22, 1 << 22, 67_108_864, 2, 8) == "rows"
+
+
+def test_schedule_units_covers_and_balances():
+    """Every unit runs exactly once (whole on one rank, or split on all ranks), big units
+    are split, and LPT keeps the per-rank load within one small unit of the ideal."""
+    from paper_2202_08556_b200 import multi
+
+    rng = np.random.default_rng(3)
+    costs = list(rng.uniform(5, 50, 60)) + [900.0, 1200.0, 400.0]
+    for parts in (1, 2, 4, 8):
+        assign, split = multi.schedule_units(costs, parts)
+        seen = {}
+        for r, units in enumerate(assign):
+            for i in units:
+                seen.setdefault(i, []).append(r)
+        assert sorted(seen) == list(range(len(costs)))
+        for i, ranks in seen.items():
+            assert (sorted(ranks) == list(range(parts))) if split[i] else len(ranks) == 1
+        loads = [sum(costs[i] / parts if split[i] else costs[i] for i in units)
+                 for units in assign]
+        ideal = sum(costs) / parts
+        assert max(loads) <= ideal + 50.0
+        if parts > 1:
+            assert split[-2]  # the largest unit always exceeds half a rank's share
+        if parts >= 4:
+            assert split[-3]
+        if parts >= 8:
+            assert split[-1]
+    assert multi.schedule_units([1.0, 2.0], 1) == ([[0, 1]], [False, False])
