@@ -191,7 +191,8 @@ int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, 
  *   variant 0 = the design point's base kernel, 1 = RB+SR with the B window staged in
  *   shared memory (*param = rows per CTA panel), 2 = EB+SR with CTA-combined boundary
  *   rows, 3 = EB+SR one-lane staged sub-chunks (*param = pairs per thread), 4 = lean
- *   SR kernel (*param = rows per group for RB, pairs per chunk for EB).
+ *   SR kernel (*param = rows per group for RB, pairs per chunk for EB), 5 = EB+SR with
+ *   TMA gather4 B-row fetches (*param = pairs per warp).
  * Diagnostics for tests and the bench's per-call report. */
 int daspmm_plan_info(const daspmm_csr* csr, int kernel, int64_t N, const void* d_B, int64_t ldb,
                      const void* d_C, int64_t ldc, unsigned flags, int* variant, int64_t* param);

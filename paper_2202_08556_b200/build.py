@@ -30,9 +30,9 @@ CFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcom
                  "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 
 LIB_SOURCES = ["abi.cu", "features.cu", "select.cu", "graph.cu", "spmm_rb_sr.cu",
-               "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu"]
+               "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu", "spmm_tma.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "dispatch.h", "internal.h", "launch_sr.cuh",
-           "launch_pr.cuh", "lean.cuh"]
+           "launch_pr.cuh", "lean.cuh", "tma_gather.cuh"]
 
 
 def _mtime(p):

@@ -242,6 +242,20 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     }
     const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
     int64_t workers;
+    // TMA gather4 EB kernel (opt-in while being measured: DASPMM_TMA=1)
+    if (eb && p.lean && N >= 32 && getenv("DASPMM_TMA") && getenv("DASPMM_TMA")[0] == '1' &&
+        tma_gather_supported(B, ldb, N, h->K) && h->nnz < (int64_t(1) << 31) - 1024) {
+        p.tma = true;
+        p.lean = false;
+        const int bc = tma_box_cols(N);
+        p.sub = 256;  // Lw: nonzeros per warp (multiple of 16)
+        const char* lw = getenv("DASPMM_TMA_LW");
+        if (lw && atoi(lw) >= 16) p.sub = (atoi(lw) / 16) * 16;
+        p.P = (h->nnz + p.sub - 1) / p.sub;  // warps
+        p.grid = dim3(unsigned((p.P + kTmaWarpsHost - 1) / kTmaWarpsHost),
+                      unsigned((N + bc - 1) / bc), 1);
+        return p;
+    }
     if (eb && p.lean) {
         // short rows: range walk (COO ids per block); long rows: segment walk.
         // DASPMM_LEAN_RW=0/1 forces one (tuning aid).
@@ -347,6 +361,13 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
                    reinterpret_cast<uintptr_t>(h->coo_rows)) & 15) == 0) ? 1 : 0;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if constexpr (std::is_same<T, float>::value) {
+        if (p.tma) {  // prologue: split rows at warp-range ends and empty rows
+            cudaError_t e = launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, 1,
+                                                      static_cast<T*>(C), ldc, int(N),
+                                                      h->empty_rows, int(h->n_empty), s);
+            if (e != cudaSuccess) return e;
+            return launch_eb_sr_tma(p, a, s);
+        }
         if (p.lean) {
             if (eb) {  // prologue: split rows at chunk ends and empty rows are zeroed
                 cudaError_t e = launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, 1,
@@ -809,8 +830,8 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
     if (kernel < 0 || kernel > 7) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
     if (int rc = ensure_coo(h, 0)) return rc;
     const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
-    *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : 0;
-    *param = p.win_rows > 0 ? p.win_rows : (p.thr || (p.lean && kernel >= 4)) ? p.sub
+    *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
+    *param = p.win_rows > 0 ? p.win_rows : (p.thr || p.tma || (p.lean && kernel >= 4)) ? p.sub
              : p.lean ? p.rpg : 0;
     return DASPMM_OK;
 }

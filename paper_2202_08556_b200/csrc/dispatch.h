@@ -25,6 +25,7 @@ struct Plan {
     int64_t sub = 0;     // ... its pairs per group sub-chunk
     bool lean = false;   // RB/EB+RM+SR lean kernels (lean.cuh), fp32 fast mode
     bool lean_rw = false;  // ... EB: range walk with COO row ids (short rows)
+    bool tma = false;    // EB+RM+SR with TMA gather4 B-row fetches (tma_gather.cuh)
     int win_rows = 0;    // RB+SR window kernel (k_rb_sr_win): rows per CTA panel, 0 = off
     size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
 };
@@ -33,6 +34,7 @@ struct Plan {
 // s20): V <= 2 takes 12 (4 x odd: 128-bit conflict-free shared reads; N = 2 129 -> 105
 // us), V = 4 keeps 7 (odd, scalar reads; 12 spent 80 registers and ran 126 -> 150 us).
 constexpr int kThrS = 12;
+constexpr int kTmaWarpsHost = 4;  // == kTmaWarps (tma_gather.cuh)
 constexpr int kThrS4 = 7;
 
 // Largest dynamic shared memory of the RB window kernel (B window + alignment lead);
@@ -41,6 +43,9 @@ constexpr size_t kWinSmemMax = 72 * 1024;
 
 // Each returns cudaErrorNotSupported for a shape with no instantiation.
 cudaError_t launch_sr_lean(const Plan&, const SpmmArgs<float>&, cudaStream_t);
+cudaError_t launch_eb_sr_tma(const Plan&, const SpmmArgs<float>&, cudaStream_t);
+bool tma_gather_supported(const void* B, int64_t ldb, int64_t N, int64_t K);
+int tma_box_cols(int64_t N);
 template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);

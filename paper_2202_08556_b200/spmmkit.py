@@ -379,7 +379,7 @@ def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int 
     return C_out
 
 
-PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean"}
+PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma"}
 
 
 def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False):

@@ -512,3 +512,36 @@ def test_lean_sr_kernels(sk, kernel, skew):
             err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
             assert (err <= bound).all(), f"k{kernel} n{n} padded={padded}: {np.nanmax(err)}"
     assert "lean" in seen
+
+
+@pytest.mark.parametrize("skew", [0.0, 1.3])
+def test_eb_tma_gather_kernel(sk, skew):
+    """EB+RM+SR with TMA gather4 row fetches (DASPMM_TMA=1): box widths 32/64/128 with
+    zero-filled columns past N, several y-tiles, padded ldb, odd nnz (array-tail stage),
+    empty rows and rows split across warp ranges; within the gamma bound."""
+    import os
+
+    import torch
+
+    a = H.random_csr(5003, 4001, 90001, seed=21, dtype=np.float32, skew=skew)
+    d = sk.DeviceCsr.from_host(a)
+    os.environ["DASPMM_TMA"] = "1"
+    try:
+        for n in (32, 40, 64, 100, 128, 256, 300):
+            x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
+            y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+            bound = H.gamma_bound(a, x, np.float32)
+            for padded in (False, True):
+                if padded:
+                    B = torch.zeros(a.num_cols, n + 12, device="cuda")[:, :n]
+                    B.copy_(torch.from_numpy(x))
+                else:
+                    B = torch.from_numpy(x).cuda()
+                C = torch.full((a.num_rows, n), float("nan"), device="cuda")
+                assert sk.plan_info(4, d, B, C)[0] == "eb_tma", n
+                sk.spmm_device(4, d, B, C)
+                torch.cuda.synchronize()
+                err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+                assert (err <= bound).all(), f"n{n} padded={padded}: {np.nanmax(err)}"
+    finally:
+        del os.environ["DASPMM_TMA"]
