@@ -435,6 +435,8 @@ int check_call(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb
     (void)exact;
     if (N < 0) return fail(DASPMM_ERR_DIMS, "spmm: negative N");
     if (N > (int64_t(1) << 30)) return fail(DASPMM_ERR_UNSUPPORTED, "spmm: N too large");
+    if (!((kernel >> 1) & 1) && ldb > (int64_t(1) << 27))  // row pitch in bytes fits int32
+        return fail(DASPMM_ERR_UNSUPPORTED, "spmm: ldb too large for row-major B");
     const bool want_cm = (kernel >> 1) & 1;
     if ((b_layout == DASPMM_COL_MAJOR) != want_cm)
         return fail(DASPMM_ERR_LAYOUT, std::string("spmm: kernel ") + kKernelNames[kernel] +

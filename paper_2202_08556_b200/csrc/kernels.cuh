@@ -165,6 +165,12 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
         }
     };
 
+    // Row-major gathers: per-slot byte base &B[0][col] and a 32-bit row pitch in bytes,
+    // so each gather address is one IMAD.WIDE (ldb * sizeof(T) < 2^31, plan_spmm).
+    const char* Bcol[CPL];
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) Bcol[s] = reinterpret_cast<const char*>(a.B + n0 + s * LPR * V);
+    const int ldb_bytes = int(a.ldb) * int(sizeof(T));
     int c[EPL], rr[EB ? EPL : 1];
     T v[EPL];
     auto load_step = [&](int j, int* cc, T* vvv, int* rrr) {
@@ -206,8 +212,12 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                             if (col < a.N)
                                 b[u][s] = ld_frag_shared<T, V>(win.s + int64_t(k) * win.pitch +
                                                                (col - win.tile0));
-                        } else {
+                        } else if constexpr (CM) {
                             if (col < a.N) b[u][s] = gather<T, CM, V>(a, u < nb ? ct : 0, col);
+                        } else {
+                            if (col < a.N)
+                                b[u][s] = ld_frag<T, V>(reinterpret_cast<const T*>(
+                                    Bcol[s] + int64_t(u < nb ? ct : 0) * ldb_bytes));
                         }
                     }
                 }
