@@ -167,9 +167,14 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 
     // Row-major gathers: per-slot byte base &B[0][col] and a 32-bit row pitch in bytes,
     // so each gather address is one IMAD.WIDE (ldb * sizeof(T) < 2^31, plan_spmm).
+    // Lanes past N gather column 0 instead (always in bounds, never stored), so the
+    // gathers need no predicate — predicated vector loads cost a register copy each.
     const char* Bcol[CPL];
 #pragma unroll
-    for (int s = 0; s < CPL; ++s) Bcol[s] = reinterpret_cast<const char*>(a.B + n0 + s * LPR * V);
+    for (int s = 0; s < CPL; ++s) {
+        const int col = n0 + s * LPR * V;
+        Bcol[s] = reinterpret_cast<const char*>(a.B + (col < a.N ? col : 0));
+    }
     const int ldb_bytes = int(a.ldb) * int(sizeof(T));
     int c[EPL], rr[EB ? EPL : 1];
     T v[EPL];
@@ -215,9 +220,9 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                         } else if constexpr (CM) {
                             if (col < a.N) b[u][s] = gather<T, CM, V>(a, u < nb ? ct : 0, col);
                         } else {
-                            if (col < a.N)
-                                b[u][s] = ld_frag<T, V>(reinterpret_cast<const T*>(
-                                    Bcol[s] + int64_t(u < nb ? ct : 0) * ldb_bytes));
+                            (void)col;
+                            b[u][s] = ld_frag<T, V>(reinterpret_cast<const T*>(
+                                Bcol[s] + int64_t(u < nb ? ct : 0) * ldb_bytes));
                         }
                     }
                 }
