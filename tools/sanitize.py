@@ -18,7 +18,7 @@ for dtype in (np.float32, np.float64):
     a = H.random_csr(700, 600, 9000, seed=4, dtype=dtype, skew=1.4)
     d = sk.DeviceCsr.from_host(a)
     tdt = torch.float32 if dtype == np.float32 else torch.float64
-    for n in (1, 3, 8, 33, 128):
+    for n in (1, 2, 3, 4, 8, 16, 33, 64, 128):
         B = torch.rand(600, n, dtype=tdt, device="cuda")
         Bcm = B.t().contiguous()
         C = torch.empty(700, n, dtype=tdt, device="cuda")
@@ -31,5 +31,28 @@ for dtype in (np.float32, np.float64):
             kout = torch.zeros(1, dtype=torch.int32, device="cuda")
             sk.spmm_selected(d, model, B, C, kernel_out=kout)
             sk.spmm_selected(d, model, B, C, kernel_out=kout)
+# opt-in launch variants: TMA gather4 EB kernel, shared-memory B window (banded input)
+a = H.random_csr(700, 600, 9001, seed=5, dtype=np.float32, skew=1.2)
+d = sk.DeviceCsr.from_host(a)
+os.environ["DASPMM_TMA"] = "1"
+for n in (32, 64, 100, 128):
+    B = torch.rand(600, n, device="cuda")
+    C = torch.empty(700, n, device="cuda")
+    sk.spmm_device(4, d, B, C)
+del os.environ["DASPMM_TMA"]
+rows = np.repeat(np.arange(2000), 9)
+cols = rows + np.tile(np.arange(-4, 5), 2000)
+keep = (cols >= 0) & (cols < 2000)
+rp = np.concatenate([[0], np.cumsum(np.bincount(rows[keep], minlength=2000))]).astype(np.int64)
+band = sk.CsrMatrix(2000, 2000, rp, cols[keep].astype(np.int64),
+                    np.random.default_rng(1).uniform(-1, 1, keep.sum()).astype(np.float32),
+                    np.float32)
+d = sk.DeviceCsr.from_host(band)
+os.environ["DASPMM_WIN"] = "1"
+for n in (2, 8, 32, 128):
+    B = torch.rand(2000, n, device="cuda")
+    C = torch.empty(2000, n, device="cuda")
+    sk.spmm_device(0, d, B, C)
+del os.environ["DASPMM_WIN"]
 torch.cuda.synchronize()
 print("sanitize driver done")
