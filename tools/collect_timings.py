@@ -26,7 +26,7 @@ def corpus(quick: bool):
     specs = []
     scales = range(10, 21) if not quick else (10, 14, 17)
     for s in scales:
-        for deg in (2, 8, 32) if not quick else (8,):
+        for deg in (2, 8, 16, 32) if not quick else (8,):
             if (1 << s) * deg > 40_000_000:
                 continue
             specs.append(("uniform", s, deg, None))
