@@ -230,12 +230,21 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
              p.L >= lean_min_lanes() && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
              (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
                                            reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
-    // Row-local matrices (narrow column windows, e.g. banded) keep k_rb_sr from N = 32
-    // on: its shuffle-broadcast walk reuses L1-resident B rows better (measured: banded
-    // s20 N = 32 188 vs 211 us, N = 128 582 vs 606 us).
-    if (p.lean && !eb && N >= 32 && h->span_avg[0] > 0 &&
-        h->span_avg[0] < 8.0 * double(h->nnz) / double(std::max<int64_t>(h->M, 1)))
-        p.lean = false;
+    // Where the lean walks win (measured on B200 against the shuffle-broadcast walks with
+    // their one-IMAD gather addressing, profiles/r01_notes.md step 17):
+    //   RB: nowhere by more than noise (uniform s20 N = 8 130 vs 134 us; N = 128 1246 vs
+    //       1229), so k_rb_sr keeps RB unless DASPMM_LEAN_RB=1;
+    //   EB: N <= 32 (power-law s20 N = 8 160 vs 279, N = 16 199 vs 269) and long rows at
+    //       any N (c3 3.77 vs 3.99 ms); from N = 64 on short rows the CTA-combined walk
+    //       wins (power-law s20 N = 128 799 vs 957, c4 N = 64 2.17 vs 2.45 ms).
+    const double avg_nonempty =
+        h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty) : 0.0;
+    const bool lean_ok = p.lean;  // eligibility (also of the TMA-gather variant)
+    if (p.lean && !eb) {
+        const char* e = getenv("DASPMM_LEAN_RB");
+        p.lean = e && e[0] == '1';
+    }
+    if (p.lean && eb && N > 32 && avg_nonempty < 48.0) p.lean = false;
     if (p.lean) {
         p.X = 1;
         tile_cols = int64_t(p.L) * p.V;
@@ -243,7 +252,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
     int64_t workers;
     // TMA gather4 EB kernel (opt-in while being measured: DASPMM_TMA=1)
-    if (eb && p.lean && N >= 32 && getenv("DASPMM_TMA") && getenv("DASPMM_TMA")[0] == '1' &&
+    if (eb && lean_ok && N >= 32 && getenv("DASPMM_TMA") && getenv("DASPMM_TMA")[0] == '1' &&
         tma_gather_supported(B, ldb, N, h->K) && h->nnz < (int64_t(1) << 31) - 1024) {
         p.tma = true;
         p.lean = false;
@@ -260,12 +269,9 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // short rows: range walk (COO ids per block); long rows: segment walk.
         // DASPMM_LEAN_RW=0/1 forces one (tuning aid).
         const char* rw = getenv("DASPMM_LEAN_RW");
-        const double avg_nonempty = h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty)
-                                                      : 0.0;
-        // Measured on B200 (profiles/r01_notes.md §lean): range walk wins on power-law
-        // rows up to N = 64 (s20: 342 -> 217 us at N = 16), the segment walk on long rows
-        // (c3: 5.26 -> 4.07 ms) and at N = 128.
-        p.lean_rw = rw ? rw[0] == '1' : (avg_nonempty < 48.0 && N <= 64);
+        // Measured on B200: the range walk wins on short rows (power-law s20 N = 16:
+        // 342 -> 217 us), the segment walk on long rows (c3: 5.26 -> 4.07 ms).
+        p.lean_rw = rw ? rw[0] == '1' : avg_nonempty < 48.0;
         p.sub = lean_chunk(p.lean_rw);
         // small matrices: shorten chunks until there are >= 4 CTAs per SM (s14 power-law,
         // N = 128: 128 CTAs at 256 pairs -> 88 us, vs 32 us with the grid filled)

@@ -492,9 +492,12 @@ def test_lean_sr_kernels(sk, kernel, skew):
     several y-tiles and padded ldb; within the gamma bound, every output written."""
     import torch
 
+    import os
+
     a = H.random_csr(5003, 4001, 90001, seed=11 + kernel, dtype=np.float32, skew=skew)
     d = sk.DeviceCsr.from_host(a)
     seen = set()
+    os.environ["DASPMM_LEAN_RB"] = "1"  # RB lean walk is opt-in (plan reads it per call)
     for n in (8, 16, 24, 32, 64, 96, 128, 200, 256):
         x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
         y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
@@ -511,6 +514,7 @@ def test_lean_sr_kernels(sk, kernel, skew):
             torch.cuda.synchronize()
             err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
             assert (err <= bound).all(), f"k{kernel} n{n} padded={padded}: {np.nanmax(err)}"
+    del os.environ["DASPMM_LEAN_RB"]
     assert "lean" in seen
 
 

@@ -31,7 +31,15 @@ for dtype in (np.float32, np.float64):
             kout = torch.zeros(1, dtype=torch.int32, device="cuda")
             sk.spmm_selected(d, model, B, C, kernel_out=kout)
             sk.spmm_selected(d, model, B, C, kernel_out=kout)
-# opt-in launch variants: TMA gather4 EB kernel, shared-memory B window (banded input)
+# opt-in launch variants: lean RB walk, TMA gather4 EB kernel, shared-memory B window
+os.environ["DASPMM_LEAN_RB"] = "1"
+a = H.random_csr(700, 600, 9000, seed=4, dtype=np.float32, skew=1.4)
+d = sk.DeviceCsr.from_host(a)
+for n in (8, 16, 33, 128):
+    B = torch.rand(600, n, device="cuda")
+    C = torch.empty(700, n, device="cuda")
+    sk.spmm_device(0, d, B, C)
+del os.environ["DASPMM_LEAN_RB"]
 a = H.random_csr(700, 600, 9001, seed=5, dtype=np.float32, skew=1.2)
 d = sk.DeviceCsr.from_host(a)
 os.environ["DASPMM_TMA"] = "1"
