@@ -14,10 +14,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "{" > $out/ncu_${tag}_traffic.json
 first=1
 # kernel-regex  matrix  N  kernel-id  [workload]
-for spec in "k_rb_sr_lean uniform_s20_d16 128 0" "k_eb_sr_lean powerlaw_s20_d16 128 4" \
+for spec in "k_rb_sr uniform_s20_d16 128 0" "k_eb_sr_cta powerlaw_s20_d16 128 4" \
             "k_eb_sr_lean_rw powerlaw_s20_d16 16 4" "k_eb_sr_thr uniform_s20_d16 2 4" \
-            "k_rb_sr banded_s20_b8 128 0" "k_eb_pr powerlaw_s20_d16 8 5" \
-            "k_eb_sr_lean c3_reddit_like 128 4 c3"; do
+            "k_rb_sr banded_s20_b8 128 0" "k_eb_sr_lean c3_reddit_like 128 4 c3" \
+            "k_eb_prep_uniform powerlaw_s20_d16 64 4"; do
   set -- $spec
   wl=${5:-suite}
   case_name="$2/N$3"
