@@ -549,3 +549,29 @@ def test_eb_tma_gather_kernel(sk, skew):
                 assert (err <= bound).all(), f"n{n} padded={padded}: {np.nanmax(err)}"
     finally:
         del os.environ["DASPMM_TMA"]
+
+
+def test_gcn_layer_matches_dense_reference(sk):
+    """GCN aggregation through DA-SpMM (BASELINE configs[2] shape, scaled down): the
+    normalised adjacency and a two-layer forward pass against dense fp64 torch."""
+    import torch
+
+    from paper_2202_08556_b200 import gcn, gen
+
+    torch.manual_seed(0)
+    M, K, rp, ci, va = gen.rmat(12, 16 * 4096, 0.45, 0.22, 0.22, 0.11, seed=5)
+    g = gcn.GCNGraph(M, rp, ci)
+    A = torch.zeros(M, M, dtype=torch.float64, device="cuda")
+    r = torch.repeat_interleave(torch.arange(M, device="cuda"), (rp[1:] - rp[:-1]).long())
+    A[r, ci.long()] = 1.0
+    A += torch.eye(M, dtype=torch.float64, device="cuda")
+    dinv = A.sum(1).rsqrt()
+    Ahat = dinv[:, None] * A * dinv[None, :]
+    H = torch.randn(M, 96, device="cuda")
+    l1, l2 = gcn.GCNLayer(96, 128).cuda(), gcn.GCNLayer(128, 32, activation=None).cuda()
+    out = l2(g, l1(g, H))
+    ref = Ahat @ torch.relu(Ahat @ H.double() @ l1.weight.double() + l1.bias.double())
+    ref = ref @ l2.weight.double() + l2.bias.double()
+    torch.testing.assert_close(out.double(), ref, rtol=1e-4, atol=1e-4)
+    agg = g.aggregate(H)
+    torch.testing.assert_close(agg.double(), Ahat @ H.double(), rtol=1e-5, atol=1e-5)
