@@ -6,7 +6,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdaspmm.so")
+# DASPMM_LIB overrides the library path (tuning aid: compare builds of the same sources)
+LIB_PATH = os.environ.get("DASPMM_LIB") or os.path.join(PKG, "libdaspmm.so")
 
 OK = 0
 ERR_INVALID_CONFIG = 1

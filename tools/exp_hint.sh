@@ -1,0 +1,4 @@
+for lib in "" "DASPMM_LIB=tools/bin/libdaspmm_l2hint.so"; do
+  echo "== $lib"
+  env $lib timeout 300 python tools/probe.py --only uniform_s20_d16,powerlaw_s20_d16,uniform_s17_d16 --ns 16,32,64,128 --kernels 0,4 --no-torch 2>/dev/null
+done
