@@ -282,7 +282,15 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     } else if (eb) {
         // Measured on B200 (profiles/r01_notes.md): short chunks win — 32 pairs per
         // group (64 for full-warp SR groups), the split-row atomics are cheap.
-        const int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
+        // Re-measured after the sr_walk address fix (profiles/r01_notes.md step 19): the
+        // CTA-combined SR walk wants 256 pairs per group from N = 64 on (power-law s20
+        // N = 128 800 -> 707 us, c4 N = 64 2.17 -> 1.71 ms), capped below so small
+        // matrices keep >= 4 CTAs per SM.
+        int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
+        if (!pr && !exact && p.L >= 16) {
+            const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
+            chunk = int(std::max<int64_t>(chunk, std::min<int64_t>(256, fill)));
+        }
         p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);
         workers = p.P;
         if (!pr && !exact && P <= 0 && p.L == 1 && p.X == 1 && N <= p.V && !p.cm &&
@@ -303,7 +311,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // RB+SR row blocks (measured, profiles/r01_notes.md): one row per group for
         // narrow groups (N <= 8), ~128 pairs per group once a group spans >= 8 lanes.
         const double avg = h->M > 0 ? double(h->nnz) / double(h->M) : 0.0;
-        const double target = p.L >= 8 ? 128.0 : (p.L >= 4 ? 32.0 : 16.0);
+        const double target = p.L >= 4 ? 128.0 : 16.0;  // banded N=16: 4 rows 137 -> 123 us
         int64_t rpg = avg > 0 ? int64_t(target / avg) : 64;
         // Skewed rows: a long row already fills its group; do not stack more rows on it.
         const double sd = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
