@@ -234,9 +234,10 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     // their one-IMAD gather addressing, profiles/r01_notes.md step 17):
     //   RB: nowhere by more than noise (uniform s20 N = 8 130 vs 134 us; N = 128 1246 vs
     //       1229), so k_rb_sr keeps RB unless DASPMM_LEAN_RB=1;
-    //   EB: N <= 32 (power-law s20 N = 8 160 vs 279, N = 16 199 vs 269) and long rows at
-    //       any N (c3 3.77 vs 3.99 ms); from N = 64 on short rows the CTA-combined walk
-    //       wins (power-law s20 N = 128 799 vs 957, c4 N = 64 2.17 vs 2.45 ms).
+    //   EB: N <= 16 (power-law s20 N = 8 160 vs 279, N = 16 199 vs 240) and long rows at
+    //       any N (c3 3.77 vs 3.99 ms); from N = 32 on short rows the CTA-combined walk
+    //       with 256-pair chunks wins (power-law s20 N = 32 326 vs 271, N = 128 957 vs
+    //       699, c4 N = 64 2.45 vs 1.69 ms).
     const double avg_nonempty =
         h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty) : 0.0;
     const bool lean_ok = p.lean;  // eligibility (also of the TMA-gather variant)
@@ -244,7 +245,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         const char* e = getenv("DASPMM_LEAN_RB");
         p.lean = e && e[0] == '1';
     }
-    if (p.lean && eb && N > 32 && avg_nonempty < 48.0) p.lean = false;
+    if (p.lean && eb && N > 16 && avg_nonempty < 48.0) p.lean = false;
     if (p.lean) {
         p.X = 1;
         tile_cols = int64_t(p.L) * p.V;
@@ -283,11 +284,11 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // Measured on B200 (profiles/r01_notes.md): short chunks win — 32 pairs per
         // group (64 for full-warp SR groups), the split-row atomics are cheap.
         // Re-measured after the sr_walk address fix (profiles/r01_notes.md step 19): the
-        // CTA-combined SR walk wants 256 pairs per group from N = 64 on (power-law s20
-        // N = 128 800 -> 707 us, c4 N = 64 2.17 -> 1.71 ms), capped below so small
-        // matrices keep >= 4 CTAs per SM.
+        // CTA-combined SR walk wants 256 pairs per group from N = 32 on (power-law s20
+        // N = 128 800 -> 707 us, N = 32 328 -> 273, c4 N = 64 2.17 -> 1.71 ms), capped
+        // below so small matrices keep >= 4 CTAs per SM.
         int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
-        if (!pr && !exact && p.L >= 16) {
+        if (!pr && !exact && p.L >= 8) {
             const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
             chunk = int(std::max<int64_t>(chunk, std::min<int64_t>(256, fill)));
         }
