@@ -281,12 +281,11 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         p.P = (h->nnz + p.sub - 1) / p.sub;
         workers = std::max<int64_t>(p.P, 1);
     } else if (eb) {
-        // Measured on B200 (profiles/r01_notes.md): short chunks win — 32 pairs per
-        // group (64 for full-warp SR groups), the split-row atomics are cheap.
-        // Re-measured after the sr_walk address fix (profiles/r01_notes.md step 19): the
-        // CTA-combined SR walk wants 256 pairs per group from N = 32 on (power-law s20
-        // N = 128 800 -> 707 us, N = 32 328 -> 273, c4 N = 64 2.17 -> 1.71 ms), capped
-        // below so small matrices keep >= 4 CTAs per SM.
+        // EB chunk per group (measured on B200, profiles/r01_notes.md steps 4 and 19): 32
+        // pairs (64 for full-warp SR groups) for narrow groups and PR; from 8-lane SR
+        // groups (N >= 32) 256 pairs (power-law s20 N = 128 800 -> 707 us, N = 32
+        // 328 -> 273, c4 N = 64 2.17 -> 1.71 ms), capped so small matrices keep >= 4 CTAs
+        // per SM.
         int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
         if (!pr && !exact && p.L >= 8) {
             const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
@@ -309,10 +308,10 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             workers = p.P;
         }
     } else if (!pr) {
-        // RB+SR row blocks (measured, profiles/r01_notes.md): one row per group for
-        // narrow groups (N <= 8), ~128 pairs per group once a group spans >= 8 lanes.
+        // RB+SR row blocks (measured, profiles/r01_notes.md steps 5 and 19): one row per
+        // group for 1-2 lane groups (N <= 8), ~128 pairs per group from 4 lanes on.
         const double avg = h->M > 0 ? double(h->nnz) / double(h->M) : 0.0;
-        const double target = p.L >= 4 ? 128.0 : 16.0;  // banded N=16: 4 rows 137 -> 123 us
+        const double target = p.L >= 4 ? 128.0 : 16.0;
         int64_t rpg = avg > 0 ? int64_t(target / avg) : 64;
         // Skewed rows: a long row already fills its group; do not stack more rows on it.
         const double sd = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
