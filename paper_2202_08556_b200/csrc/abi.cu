@@ -284,11 +284,11 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // EB chunk per group (measured on B200, profiles/r01_notes.md steps 4 and 19): 32
         // pairs (64 for full-warp SR groups) for narrow groups and PR; from 8-lane SR
         // groups (N >= 32) 256 pairs (power-law s20 N = 128 800 -> 707 us, N = 32
-        // 328 -> 273, c4 N = 64 2.17 -> 1.71 ms), capped so small matrices keep >= 4 CTAs
-        // per SM.
+        // 328 -> 273, c4 N = 64 2.17 -> 1.71 ms), capped so small matrices keep >= 8 CTAs
+        // per SM below full-warp groups (power-law s17 N = 32: 73 -> 64 us), >= 4 with them.
         int chunk = pr ? std::max<int>(int(W), 32) : (p.L >= 32 ? 64 : 32);
         if (!pr && !exact && p.L >= 8) {
-            const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
+            const int64_t fill = h->nnz * p.L / (148LL * (p.L >= 32 ? 4 : 8) * kThreads);
             chunk = int(std::max<int64_t>(chunk, std::min<int64_t>(256, fill)));
         }
         p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);

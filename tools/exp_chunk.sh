@@ -1,5 +1,1 @@
-for w in "DASPMM_LEAN=1" "DASPMM_LEAN=0" "DASPMM_LEAN=0 DASPMM_EB_CHUNK=128" "DASPMM_LEAN=0 DASPMM_EB_CHUNK=256"; do
-  echo "== $w"
-  env $w timeout 300 python tools/probe.py --only powerlaw_s17_d16,powerlaw_s20_d16,uniform_s20_d16,banded_s20_b8 --ns 8,16,32 --kernels 4 --no-torch 2>/dev/null
-  env $w timeout 300 python tools/probe.py --workload c4 --ns 16 --kernels 4 --no-torch 2>/dev/null
-done
+timeout 300 python tools/probe.py --only powerlaw_s14_d16,powerlaw_s17_d16,uniform_s17_d16,powerlaw_s20_d16 --ns 32,64,128 --kernels 4 --no-torch 2>/dev/null
