@@ -226,16 +226,18 @@ def run_ours(args):
                 e.record(stream)
                 times[i].append((s, e))
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    times = [[] for _ in calls]
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-    torch.cuda.synchronize()
+    # The clock sampler starts before the warm-up: its start-up pause would otherwise
+    # leave the GPU idle (and its clocks relaxed) right before the first timed call.
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        times = [[] for _ in calls]
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             step(times)
         torch.cuda.synchronize()
