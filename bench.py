@@ -153,7 +153,10 @@ def shard_calls(mats, ns_override, rank: int, world: int):
 
     units = [(m, n) for m in mats for n in (ns_override or m["ns"])]
     costs = [multi.estimate_call_us(m["nnz_total"], n) for m, n in units]
-    assign, split = multi.schedule_units(costs, world)
+    # DASPMM_SPLIT_FRAC (default 0.5) forces more row splitting, e.g. to exercise the
+    # panel path and C assembly on 2 ranks.
+    assign, split = multi.schedule_units(costs, world,
+                                         float(os.environ.get("DASPMM_SPLIT_FRAC", "0.5")))
     panels = {}
     mine = []
     for i in assign[rank]:
@@ -276,9 +279,43 @@ def run_ours(args):
     else:
         e2e = _e2e(calls, one, stream, args, world, total_flops)
     parity = _spot_check(calls[dom]) if rank == 0 else None
+    assembly = _assembly(calls, mats, world, dev) if world > 1 else None
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-                   flush)
+                   flush, assembly)
+
+
+def _assembly(calls, mats, world, dev):
+    """C assembly, timed apart from the SpMM (optional, only where the output
+    must be assembled): the largest row-split call's panels all-gathered into the full C
+    on every rank (multi.gather_rows, NCCL over NVLink). Max over ranks."""
+    import torch
+
+    from paper_2202_08556_b200 import multi
+
+    split = [c for c in calls if c["rows"] != (0, c["m"]["M"])]
+    big = max(split, key=lambda c: c["m"]["M"] * c["n"]) if split else None
+    name = f'{big["m"]["name"]}/N{big["n"]}' if big else None
+    names = [None] * world
+    import torch.distributed as dist
+
+    dist.all_gather_object(names, name)
+    if len(set(names)) != 1 or name is None:  # every rank must join the same collective
+        return None
+    cuts = multi.row_panel_cuts(big["m"]["rp"].cpu().numpy(), world)
+    full = multi.gather_rows(big["C"], cuts)  # warm-up (communicator set-up)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    full = multi.gather_rows(big["C"], cuts)
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e), dev)
+    nbytes = full.numel() * full.element_size()
+    return {"call": name, "ms": round(ms, 4), "bytes_per_rank": nbytes,
+            "collective": "all-gather of padded row panels (multi.gather_rows)"}
 
 
 def _e2e(calls, one, stream, args, world, total_flops):
@@ -336,7 +373,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
 
 def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
             per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-            flush):
+            flush, assembly=None):
     import torch.distributed as dist
 
     from paper_2202_08556_b200 import spmmkit as sk
@@ -381,6 +418,8 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                         for c, t in zip(calls, per_call_ms)},
         "parity": parity,
     }
+    if assembly is not None:
+        result["assembly"] = assembly
     if rank == 0 and not args.no_cusparse:
         result["cusparse"] = _cusparse_compare(calls, flush, per_call_ms, ns)
     if rank == 0 and world == 1 and not args.no_cpu:
