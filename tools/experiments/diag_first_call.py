@@ -7,7 +7,7 @@ import time
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2202_08556_b200 import gen  # noqa: E402
 from paper_2202_08556_b200 import spmmkit as sk  # noqa: E402
 
