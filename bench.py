@@ -314,8 +314,30 @@ def _assembly(calls, mats, world, dev):
     torch.cuda.synchronize()
     ms = _max_over_ranks(s.elapsed_time(e), dev)
     nbytes = full.numel() * full.element_size()
-    return {"call": name, "ms": round(ms, 4), "bytes_per_rank": nbytes,
-            "collective": "all-gather of padded row panels (multi.gather_rows)"}
+    out = {"call": name, "ms": round(ms, 4), "bytes_per_rank": nbytes,
+           "collective": "all-gather of padded row panels (multi.gather_rows)"}
+    # Fused alternative (NCCL runs only, one rank per GPU): the RB+RM+SR panel kernel
+    # stores every finished row into all ranks' copies of C (symmetric memory over
+    # NVLink); its time includes the SpMM itself.
+    if dist.get_backend() == "nccl":
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            r0 = big["rows"][0]
+            Cs = symm_mem.empty(big["m"]["M"], big["n"], dtype=torch.float32, device=dev)
+            multi.spmm_rows_allgather(big["d"], big["B"], big["m"]["M"], r0, C_full=Cs)
+            torch.cuda.synchronize()
+            dist.barrier()
+            s.record()
+            multi.spmm_rows_allgather(big["d"], big["B"], big["m"]["M"], r0, C_full=Cs)
+            e.record()
+            torch.cuda.synchronize()
+            out["fused_spmm_allgather_ms"] = round(_max_over_ranks(s.elapsed_time(e), dev), 4)
+            out["fused_equals_nccl"] = bool(torch.equal(Cs, full))
+        except Exception as ex:  # never let the optional path break the bench line
+            out["fused_spmm_allgather_ms"] = None
+            out["fused_error"] = str(ex)[:200]
+    return out
 
 
 def _e2e(calls, one, stream, args, world, total_flops):

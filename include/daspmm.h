@@ -187,6 +187,14 @@ int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out);
 int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, int64_t w,
                                       double* out);
 
+/* RB+RM+SR (kernel 0, fast mode, f32) whose epilogue stores every finished row of C to
+ * n_dst destinations d_C[0..n_dst) (1 <= n_dst <= 8, all with leading dimension ldc):
+ * with destinations that are the peers' copies of an assembled C (NVLink-mapped
+ * symmetric memory), a rank's row-panel SpMM and the all-gather of its panel are one
+ * kernel (paper_2202_08556_b200.multi.spmm_rows_allgather). */
+int daspmm_spmm_rows_to(const daspmm_csr* csr, const void* d_B, int64_t ldb, int64_t N,
+                        void* const* d_C, int n_dst, int64_t ldc, daspmm_stream stream);
+
 /* Which launch variant daspmm_spmm would run for these operands (no launch):
  *   variant 0 = the design point's base kernel, 1 = RB+SR with the B window staged in
  *   shared memory (*param = rows per CTA panel), 2 = EB+SR with CTA-combined boundary

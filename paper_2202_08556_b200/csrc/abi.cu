@@ -190,7 +190,7 @@ static void plan_window(const daspmm_csr* h, Plan& p, int64_t N, int64_t tile_co
 }
 
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
-               int64_t ldb, const void* C, int64_t ldc, bool exact) {
+               int64_t ldb, const void* C, int64_t ldc, bool exact, bool base_only) {
     Plan p;
     p.kernel = kernel;
     p.cm = (kernel >> 1) & 1;
@@ -226,7 +226,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     }
     // Lean SR kernels (lean.cuh): fp32 fast mode, row-major B, groups of >= 2 lanes,
     // quad-aligned A arrays. One column slot per lane; wider N takes more y-tiles.
-    p.lean = !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 && lean_enabled() &&
+    p.lean = !base_only && !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 &&
+             lean_enabled() &&
              p.L >= lean_min_lanes() && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
              (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
                                            reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
@@ -332,7 +333,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         }
         p.rpg = rpg;
         workers = (h->M + rpg - 1) / rpg;
-        plan_window(h, p, N, tile_cols, ytiles, B, exact);
+        if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact);
         if (p.win_rows > 0) {
             p.lean = false;
             p.grid = dim3(unsigned((h->M + p.win_rows - 1) / p.win_rows), unsigned(ytiles), 1);
@@ -350,8 +351,11 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
 template <typename T>
 static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const void* B,
                             int64_t ldb, int64_t N, void* C, int64_t ldc, int* chunk_row,
-                            cudaStream_t s) {
+                            cudaStream_t s, void* const* extra = nullptr, int n_extra = 0) {
     SpmmArgs<T> a;
+    a.n_extra = n_extra;
+    for (int d = 0; d < kMaxExtraDst; ++d)
+        a.extra[d] = d < n_extra ? static_cast<T*>(extra[d]) : nullptr;
     a.rp = h->rp;
     a.ci = h->ci;
     a.va = static_cast<const T*>(h->va);
@@ -837,6 +841,34 @@ int daspmm_partition(const daspmm_csr* h, int64_t p, int64_t* begin, int64_t* en
         if (row) row[i] = rows[size_t(i)];
         start += size;
     }
+    return DASPMM_OK;
+}
+
+int daspmm_spmm_rows_to(const daspmm_csr* h, const void* B, int64_t ldb, int64_t N,
+                        void* const* C, int n_dst, int64_t ldc, daspmm_stream stream) {
+    if (!h || !C || n_dst < 1) return fail(DASPMM_ERR_INVALID_ARG, "spmm_rows_to: null argument");
+    if (n_dst > 1 + kMaxExtraDst)
+        return fail(DASPMM_ERR_UNSUPPORTED, "spmm_rows_to: at most 8 destinations");
+    if (h->dtype != DASPMM_F32)
+        return fail(DASPMM_ERR_UNSUPPORTED, "spmm_rows_to: float32 handles only");
+    for (int d = 0; d < n_dst; ++d)
+        if (!C[d]) return fail(DASPMM_ERR_INVALID_ARG, "spmm_rows_to: null destination");
+    if (int rc = check_call(h, 0, 0, 8, 8, DASPMM_ROW_MAJOR, ldb, N, ldc, false)) return rc;
+    if (h->M == 0 || N == 0) return DASPMM_OK;
+    DeviceGuard g(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    keep_pool_warm(h->device);
+    // RB+RM+SR through the shuffle-broadcast row walk (k_rb_sr): every row is owned by
+    // exactly one group, so the replicated epilogue needs plain stores only. The vector
+    // width must suit every destination, so the plan checks the least aligned one.
+    const void* worst = C[0];
+    for (int d = 1; d < n_dst; ++d)
+        if ((reinterpret_cast<uintptr_t>(C[d]) & 15) != 0) worst = C[d];
+    const Plan p = plan_spmm(h, 0, 0, 8, N, B, ldb, worst, ldc, false, /*base_only=*/true);
+    cudaError_t e = run_plan<float>(h, p, 8, B, ldb, N, C[0], ldc, nullptr, s, C + 1, n_dst - 1);
+    if (e == cudaErrorNotSupported)
+        return fail(DASPMM_ERR_UNSUPPORTED, "spmm_rows_to: no instantiation for this shape");
+    if (e != cudaSuccess) return cuda_fail(e, "spmm_rows_to");
     return DASPMM_OK;
 }
 

@@ -77,8 +77,9 @@ int ensure_coo(const daspmm_csr* h, cudaStream_t s);
 int exact_std(daspmm_csr* h, double* out);
 // Implemented in abi.cu
 struct Plan;
+// base_only: the design point's base kernel (no lean / window / TMA launch variants).
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
-               int64_t ldb, const void* C, int64_t ldc, bool exact);
+               int64_t ldb, const void* C, int64_t ldc, bool exact, bool base_only = false);
 int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const void* B,
                 int64_t ldb, int64_t N, void* C, int64_t ldc, unsigned flags, cudaStream_t s,
                 int* chunk_scratch);

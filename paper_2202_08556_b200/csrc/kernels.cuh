@@ -26,6 +26,8 @@
 
 namespace daspmm {
 
+constexpr int kMaxExtraDst = 7;  // + the primary C: up to 8 ranks on one NVSwitch box
+
 template <typename T>
 struct SpmmArgs {
     const int* __restrict__ rp;  // M+1 row offsets
@@ -44,6 +46,11 @@ struct SpmmArgs {
     const int* __restrict__ rows;       // EB: COO row id of every nonzero (handle-owned)
     const int2* __restrict__ spans;     // RB window kernel: column window per 32-row panel
     int win_rows;                       // RB window kernel: rows per CTA panel (32 << i)
+    // RB+SR replicated epilogue (daspmm_spmm_rows_to): every finished row is also stored
+    // to extra[0 .. n_extra) (same ldc) — e.g. the peers' copies of the assembled C,
+    // mapped over NVLink, so a row-panel SpMM and its all-gather are one kernel.
+    int n_extra;
+    T* extra[kMaxExtraDst];
 };
 
 constexpr int kThreads = 256;
@@ -158,9 +165,12 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                 }
             }
             if (col < a.N) {
-                T* y = a.C + int64_t(r) * a.ldc + col;
-                if (owned) st_frag(y, out);
-                else atomic_add_frag(y, out);
+                const int64_t off = int64_t(r) * a.ldc + col;
+                if (owned) st_frag(a.C + off, out);
+                else atomic_add_frag(a.C + off, out);
+                if constexpr (MODE == kRB) {
+                    for (int d = 0; d < a.n_extra; ++d) st_frag(a.extra[d] + off, out);
+                }
             }
         }
     };

@@ -18,7 +18,10 @@ loaded rank (LPT). Every unit runs on exactly one rank; there is no collective o
 data path.
 
 C stays sharded by default. `gather_rows` / `gather_cols` assemble it on every rank
-with NCCL all-gather when a consumer needs the full matrix (timed separately).
+with NCCL all-gather when a consumer needs the full matrix (timed separately), and
+`spmm_rows_allgather` fuses the assembly into the SpMM itself: C lives in symmetric
+memory, and each rank's row-panel kernel stores every finished row into all ranks'
+copies over NVLink (daspmm_spmm_rows_to) — no collective after the kernel, one barrier.
 """
 from __future__ import annotations
 
@@ -130,3 +133,35 @@ def gather_cols(local_c, bounds, group=None):
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
     return torch.cat([outs[p][:, : widths[p]] for p in range(world)], 1)
+
+
+def spmm_rows_allgather(panel, B, M: int, r0: int, group=None, C_full=None):
+    """Row-panel SpMM fused with the all-gather of C (one process per GPU, NVLink).
+
+    `panel` is this rank's DeviceCsr of rows [r0, r0 + panel.num_rows). C (M x N, fp32)
+    is allocated in PyTorch symmetric memory (or passed in, allocated that way); the
+    rank's RB+RM+SR kernel writes each finished row into every rank's copy through the
+    peer mappings, then all ranks meet at the symmetric-memory barrier. Returns the
+    assembled C on every rank."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    from . import spmmkit as sk
+
+    group = group or dist.group.WORLD
+    N = B.shape[1]
+    if C_full is None:
+        C_full = symm_mem.empty(M, N, dtype=torch.float32, device=B.device)
+    hdl = symm_mem.rendezvous(C_full, group)
+    world = dist.get_world_size(group)
+    rows = panel.num_rows
+    dsts = []
+    for q in range(world):  # own copy first (it carries the vector-width checks)
+        peer = (dist.get_rank(group) + q) % world
+        full = hdl.get_buffer(peer, (M, N), torch.float32)
+        dsts.append(full[r0:r0 + rows])
+    hdl.barrier()  # every copy is allocated before anyone writes into it
+    sk.spmm_rows_to(panel, B, dsts)
+    hdl.barrier()  # all panels have landed everywhere
+    return C_full

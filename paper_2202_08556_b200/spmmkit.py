@@ -379,6 +379,19 @@ def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int 
     return C_out
 
 
+def spmm_rows_to(a: DeviceCsr, B, outs, stream=None):
+    """RB+RM+SR with the row epilogue replicated into every tensor of `outs` (each
+    M x N row-major with the same leading dimension, fp32) — see daspmm_spmm_rows_to."""
+    outs = list(outs)
+    ldc = _ld(outs[0])
+    if any(_ld(o) != ldc or tuple(o.shape) != tuple(outs[0].shape) for o in outs):
+        raise InvalidArgument(_lib.ERR_DIMS, "spmm_rows_to: destinations differ in shape")
+    ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    check(lib().daspmm_spmm_rows_to(a._h, B.data_ptr(), _ld(B), B.shape[1], ptrs, len(outs),
+                                    ldc, _stream_ptr(stream)))
+    return outs[0]
+
+
 PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma"}
 
 

@@ -575,3 +575,31 @@ def test_gcn_layer_matches_dense_reference(sk):
     torch.testing.assert_close(out.double(), ref, rtol=1e-4, atol=1e-4)
     agg = g.aggregate(H)
     torch.testing.assert_close(agg.double(), Ahat @ H.double(), rtol=1e-5, atol=1e-5)
+
+
+def test_spmm_rows_to_replicates_rows(sk):
+    """daspmm_spmm_rows_to: the RB+RM+SR row epilogue stored into several destinations
+    (here local buffers standing in for the peers' NVLink-mapped copies of C, one of
+    them a row-offset view of a larger matrix) — every copy equals the single-
+    destination result and is within the gamma bound."""
+    import torch
+
+    a = H.random_csr(3000, 2500, 50000, seed=31, dtype=np.float32, skew=0.8)
+    d = sk.DeviceCsr.from_host(a)
+    for n in (3, 32, 100, 256):
+        x = np.random.default_rng(n).uniform(-1, 1, (2500, n)).astype(np.float32)
+        B = torch.from_numpy(x).cuda()
+        y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+        bound = H.gamma_bound(a, x, np.float32)
+        big = torch.full((3000 + 700, n), float("nan"), device="cuda")
+        outs = [torch.full((3000, n), float("nan"), device="cuda") for _ in range(2)]
+        outs.append(big[500:3500])
+        sk.spmm_rows_to(d, B, outs)
+        ref = torch.empty(3000, n, device="cuda")
+        sk.spmm_device(0, d, B, ref)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o, ref), n
+        err = np.abs(ref.cpu().numpy().astype(np.float64) - y64)
+        assert (err <= bound).all()
+        assert torch.isnan(big[:500]).all() and torch.isnan(big[3500:]).all()
