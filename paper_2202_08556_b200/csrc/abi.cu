@@ -864,7 +864,8 @@ int daspmm_spmm_rows_to(const daspmm_csr* h, const void* B, int64_t ldb, int64_t
     const void* worst = C[0];
     for (int d = 1; d < n_dst; ++d)
         if ((reinterpret_cast<uintptr_t>(C[d]) & 15) != 0) worst = C[d];
-    const Plan p = plan_spmm(h, 0, 0, 8, N, B, ldb, worst, ldc, false, /*base_only=*/true);
+    Plan p = plan_spmm(h, 0, 0, 8, N, B, ldb, worst, ldc, false, /*base_only=*/true);
+    p.repl = true;
     cudaError_t e = run_plan<float>(h, p, 8, B, ldb, N, C[0], ldc, nullptr, s, C + 1, n_dst - 1);
     if (e == cudaErrorNotSupported)
         return fail(DASPMM_ERR_UNSUPPORTED, "spmm_rows_to: no instantiation for this shape");

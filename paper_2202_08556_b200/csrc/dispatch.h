@@ -27,6 +27,7 @@ struct Plan {
     bool lean_rw = false;  // ... EB: range walk with COO row ids (short rows)
     bool tma = false;    // EB+RM+SR with TMA gather4 B-row fetches (tma_gather.cuh)
     int win_rows = 0;    // RB+SR window kernel (k_rb_sr_win): rows per CTA panel, 0 = off
+    bool repl = false;   // RB+SR with the replicated row epilogue (daspmm_spmm_rows_to)
     size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
 };
 

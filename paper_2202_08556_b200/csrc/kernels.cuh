@@ -46,9 +46,10 @@ struct SpmmArgs {
     const int* __restrict__ rows;       // EB: COO row id of every nonzero (handle-owned)
     const int2* __restrict__ spans;     // RB window kernel: column window per 32-row panel
     int win_rows;                       // RB window kernel: rows per CTA panel (32 << i)
-    // RB+SR replicated epilogue (daspmm_spmm_rows_to): every finished row is also stored
-    // to extra[0 .. n_extra) (same ldc) — e.g. the peers' copies of the assembled C,
-    // mapped over NVLink, so a row-panel SpMM and its all-gather are one kernel.
+    // RB+SR replicated epilogue (k_rb_sr<..., kRBRepl>, daspmm_spmm_rows_to): every
+    // finished row is also stored to extra[0 .. n_extra) (same ldc) — e.g. the peers'
+    // copies of the assembled C mapped over NVLink, so a row-panel SpMM and its
+    // all-gather are one kernel.
     int n_extra;
     T* extra[kMaxExtraDst];
 };
@@ -89,7 +90,7 @@ struct CtaSlots {
     int tn = 0;          // tile width
 };
 
-enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2, kRBWin = 3 };
+enum WalkMode { kRB = 0, kEB = 1, kEBCta = 2, kRBWin = 3, kRBRepl = 4 };
 
 // RB window kernel: the CTA's B rows [c0, c0 + span) staged in shared memory, `pitch`
 // elements per row starting at column tile0.
@@ -168,7 +169,7 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
                 const int64_t off = int64_t(r) * a.ldc + col;
                 if (owned) st_frag(a.C + off, out);
                 else atomic_add_frag(a.C + off, out);
-                if constexpr (MODE == kRB) {
+                if constexpr (MODE == kRBRepl) {  // replicated epilogue (daspmm_spmm_rows_to)
                     for (int d = 0; d < a.n_extra; ++d) st_frag(a.extra[d] + off, out);
                 }
             }
@@ -306,7 +307,9 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 }
 
 // RB + SR: group g owns rows [g*rpg, (g+1)*rpg) — a row block (rpg <= LPR).
-template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL>
+// MODE kRBRepl adds the replicated row epilogue (a separate instantiation, so the
+// common path carries none of it).
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE = kRB>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4) k_rb_sr(const SpmmArgs<T> a) {
     constexpr int TN = LPR * V * CPL;
     const unsigned mask = group_mask<LPR>();
@@ -316,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     if (r0 >= a.M) return;  // whole group leaves together
     const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
     const int n0 = blockIdx.y * TN + gl * V;
-    sr_walk<T, CM, EXACT, V, LPR, CPL, kRB>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0),
-                                            r1 - int(r0), n0, mask, gl);
+    sr_walk<T, CM, EXACT, V, LPR, CPL, MODE>(a, __ldg(a.rp + r0), __ldg(a.rp + r1), int(r0),
+                                             r1 - int(r0), n0, mask, gl);
 }
 
 // RB + SR with the B window in shared memory (row-local matrices: banded, meshes).

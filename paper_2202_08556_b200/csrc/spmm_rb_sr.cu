@@ -50,8 +50,36 @@ static cudaError_t launch_rb_sr_win(const Plan& p, const SpmmArgs<float>& a, cud
     }
 }
 
+// Replicated row epilogue (fp32 fast mode, row-major B): the k_rb_sr table with
+// MODE = kRBRepl.
+#define DASPMM_REPL_LPR_TABLE(V)                                                       \
+    switch (p.L) {                                                                    \
+        case 1: k_rb_sr<float, false, false, V, 1, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); break; \
+        case 2: k_rb_sr<float, false, false, V, 2, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); break; \
+        case 4: k_rb_sr<float, false, false, V, 4, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); break; \
+        case 8: k_rb_sr<float, false, false, V, 8, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); break; \
+        case 16: k_rb_sr<float, false, false, V, 16, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); break; \
+        case 32:                                                                      \
+            if (p.X == 2) k_rb_sr<float, false, false, V, 32, 2, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); \
+            else k_rb_sr<float, false, false, V, 32, 1, kRBRepl><<<p.grid, kThreads, 0, s>>>(a); \
+            break;                                                                    \
+        default: return cudaErrorNotSupported;                                        \
+    }
+
+static cudaError_t launch_rb_sr_repl(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.cm || p.exact) return cudaErrorNotSupported;
+    switch (p.V) {
+        case 1: { DASPMM_REPL_LPR_TABLE(1) } break;
+        case 2: { DASPMM_REPL_LPR_TABLE(2) } break;
+        case 4: { DASPMM_REPL_LPR_TABLE(4) } break;
+        default: return cudaErrorNotSupported;
+    }
+    return cudaGetLastError();
+}
+
 template <>
 cudaError_t launch_rb_sr<float>(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.repl) return launch_rb_sr_repl(p, a, s);
     if (p.win_rows > 0 && !p.cm && !p.exact) return launch_rb_sr_win(p, a, s);
     return launch_rb_sr_rows<float>(p, a, s);
 }

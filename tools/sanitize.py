@@ -62,5 +62,10 @@ for n in (2, 8, 32, 128):
     C = torch.empty(2000, n, device="cuda")
     sk.spmm_device(0, d, B, C)
 del os.environ["DASPMM_WIN"]
+# replicated RB+RM+SR epilogue (fused row-panel SpMM + all-gather), three destinations
+for n in (3, 32, 128):
+    B = torch.rand(2000, n, device="cuda")
+    outs = [torch.empty(2000, n, device="cuda") for _ in range(3)]
+    sk.spmm_rows_to(d, B, outs)
 torch.cuda.synchronize()
 print("sanitize driver done")
