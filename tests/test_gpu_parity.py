@@ -603,3 +603,49 @@ def test_spmm_rows_to_replicates_rows(sk):
         err = np.abs(ref.cpu().numpy().astype(np.float64) - y64)
         assert (err <= bound).all()
         assert torch.isnan(big[:500]).all() and torch.isnan(big[3500:]).all()
+
+
+@pytest.mark.parametrize("case", ["one_nnz", "three_nnz", "all_empty_but_last", "single_long_row",
+                                  "chunk_aligned_rows"])
+def test_fast_paths_edge_shapes(sk, case):
+    """Edge shapes through every fp32 fast path (lean walks, one-lane staged path, CTA-
+    combined walk, replicated epilogue): nnz below one quad, a matrix whose nonzeros all
+    sit in its last row, one row longer than every chunk, and rows ending exactly on
+    chunk boundaries. Every output element written (NaN-poisoned), gamma bound held."""
+    import torch
+
+    from paper_2202_08556_b200.spmmkit import CsrMatrix
+
+    rng = np.random.default_rng(7)
+    if case == "one_nnz":
+        M, K, lens = 5, 7, [0, 0, 1, 0, 0]
+    elif case == "three_nnz":
+        M, K, lens = 3, 9, [1, 0, 2]
+    elif case == "all_empty_but_last":
+        M, K, lens = 4000, 300, [0] * 3999 + [300]
+    elif case == "single_long_row":
+        M, K, lens = 64, 70000, [3] * 31 + [60000] + [5] * 32
+    else:  # every row holds 128 nonzeros: rows end on every chunk boundary
+        M, K, lens = 2048, 4096, [128] * 2048
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(K, size=l, replace=False)) if l else
+                         np.zeros(0, np.int64) for l in lens]).astype(np.int64)
+    a = CsrMatrix(M, K, rp, ci, rng.uniform(-1, 1, ci.size).astype(np.float32), np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    for n in (1, 2, 4, 8, 16, 32, 64, 128):
+        x = rng.uniform(-1, 1, (K, n)).astype(np.float32)
+        B = torch.from_numpy(x).cuda()
+        y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+        bound = H.gamma_bound(a, x, np.float32)
+        for k in (0, 4):
+            C = torch.full((M, n), float("nan"), device="cuda")
+            sk.spmm_device(k, d, B, C)
+            torch.cuda.synchronize()
+            err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= bound).all(), f"{case} k{k} n{n}: {np.nanmax(err)}"
+        outs = [torch.full((M, n), float("nan"), device="cuda") for _ in range(2)]
+        sk.spmm_rows_to(d, B, outs)
+        torch.cuda.synchronize()
+        for o in outs:
+            err = np.abs(o.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= bound).all(), f"{case} rows_to n{n}"
