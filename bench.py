@@ -279,7 +279,12 @@ def run_ours(args):
     else:
         e2e = _e2e(calls, one, stream, args, world, total_flops)
     parity = _spot_check(calls[dom]) if rank == 0 else None
-    assembly = _assembly(calls, mats, world, dev) if world > 1 else None
+    assembly = None
+    if world > 1:
+        try:
+            assembly = _assembly(calls, mats, world, dev)
+        except Exception as ex:  # optional measurement: never lose the bench line to it
+            assembly = {"error": str(ex)[:200]}
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
                    flush, assembly)
@@ -302,6 +307,10 @@ def _assembly(calls, mats, world, dev):
     dist.all_gather_object(names, name)
     if len(set(names)) != 1 or name is None:  # every rank must join the same collective
         return None
+    full_bytes = big["m"]["M"] * big["n"] * 4
+    if full_bytes > (8 << 30):  # c5: 34 GB per GPU, more than the SpMM itself moves
+        return {"call": name, "ms": None, "bytes_per_rank": full_bytes,
+                "skipped": "assembled C above 8 GB per GPU"}
     cuts = multi.row_panel_cuts(big["m"]["rp"].cpu().numpy(), world)
     full = multi.gather_rows(big["C"], cuts)  # warm-up (communicator set-up)
     torch.cuda.synchronize()
