@@ -189,6 +189,27 @@ static void plan_window(const daspmm_csr* h, Plan& p, int64_t N, int64_t tile_co
     }
 }
 
+// Self-test fault hook (the reference's `validate --inject-fault`, spmmkit_cli.cpp:
+// 366-371, 394-397): with SPMMKIT_ENABLE_FAULT_INJECTION=1 and DASPMM_INJECT_FAULT=1 every
+// device SpMM adds 1 to C[0][0], so tests can prove the parity checks catch a wrong
+// result. Read per call; never set in normal use.
+static bool fault_injection_armed() {
+    const char* en = getenv("SPMMKIT_ENABLE_FAULT_INJECTION");
+    const char* f = getenv("DASPMM_INJECT_FAULT");
+    return en && en[0] == '1' && f && f[0] == '1';
+}
+
+template <typename T>
+__global__ void k_inject_fault(T* c) {
+    c[0] += T(1);
+}
+
+static cudaError_t inject_fault(int dtype, void* C, cudaStream_t s) {
+    if (dtype == DASPMM_F64) k_inject_fault<double><<<1, 1, 0, s>>>(static_cast<double*>(C));
+    else k_inject_fault<float><<<1, 1, 0, s>>>(static_cast<float*>(C));
+    return cudaGetLastError();
+}
+
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
                int64_t ldb, const void* C, int64_t ldc, bool exact, bool base_only) {
     Plan p;
@@ -437,6 +458,7 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     e = h->dtype == DASPMM_F64 ? run_plan<double>(h, p, W, B, ldb, N, C, ldc, chunk_row, s)
                                : run_plan<float>(h, p, W, B, ldb, N, C, ldc, chunk_row, s);
     if (chunk_row && own_scratch) cudaFreeAsync(chunk_row, s);
+    if (e == cudaSuccess && fault_injection_armed()) e = inject_fault(h->dtype, C, s);
     if (e == cudaErrorNotSupported)
         return fail(DASPMM_ERR_UNSUPPORTED, std::string("spmm: no instantiation for kernel ") +
                                                 kKernelNames[kernel]);

@@ -649,3 +649,35 @@ def test_fast_paths_edge_shapes(sk, case):
         for o in outs:
             err = np.abs(o.cpu().numpy().astype(np.float64) - y64)
             assert (err <= bound).all(), f"{case} rows_to n{n}"
+
+
+def test_fault_injection_is_caught(sk):
+    """Failure detection (reference: validate --inject-fault, spmmkit_cli.cpp:366-371,
+    394-397, and the zero-returning stub of test_bench.cpp:86-100): with the env-guarded
+    hook armed, a device SpMM returns a result off by 1 in C[0][0] and the gamma-bound
+    parity check rejects it; disarmed, the same check passes."""
+    import os
+
+    import torch
+
+    a = H.random_csr(300, 200, 3000, seed=2, dtype=np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    x = np.random.default_rng(1).uniform(-1, 1, (200, 16)).astype(np.float32)
+    y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+    bound = H.gamma_bound(a, x, np.float32)
+    B = torch.from_numpy(x).cuda()
+
+    def run():
+        C = torch.empty(300, 16, device="cuda")
+        sk.spmm_device(0, d, B, C)
+        torch.cuda.synchronize()
+        return bool((np.abs(C.cpu().numpy().astype(np.float64) - y64) <= bound).all())
+
+    assert run()
+    os.environ["SPMMKIT_ENABLE_FAULT_INJECTION"] = "1"
+    os.environ["DASPMM_INJECT_FAULT"] = "1"
+    try:
+        assert not run()
+    finally:
+        del os.environ["SPMMKIT_ENABLE_FAULT_INJECTION"], os.environ["DASPMM_INJECT_FAULT"]
+    assert run()
