@@ -309,8 +309,12 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 // RB + SR: group g owns rows [g*rpg, (g+1)*rpg) — a row block (rpg <= LPR).
 // MODE kRBRepl adds the replicated row epilogue (a separate instantiation, so the
 // common path carries none of it).
+// Resident CTAs per SM (measured, profiles/r01c_minblocks_probe.txt): 5 for groups of
+// >= 16 lanes (48 registers; uniform s20 N = 128 1229 -> 1210 us), 4 below (5 costs
+// N = 16 184 -> 221 us), 3 for narrow groups and fp64.
 template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE = kRB>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4) k_rb_sr(const SpmmArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : (LPR >= 16 ? 5 : 4))
+k_rb_sr(const SpmmArgs<T> a) {
     constexpr int TN = LPR * V * CPL;
     const unsigned mask = group_mask<LPR>();
     const int gl = threadIdx.x & (LPR - 1);
