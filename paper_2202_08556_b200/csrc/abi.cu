@@ -107,9 +107,11 @@ static int64_t max_tile_cols(const daspmm_csr* h, int64_t N) {
     }();
     if (env > 0) return env;
     // Measured on B200 (profiles/r01_notes.md): narrowing tiles to keep B in L2 costs
-    // more in A re-reads and shorter gathers than it saves, up to N = 128.
+    // more in A re-reads and shorter gathers than it saves, up to N = 128. Wider N runs
+    // 128-column y-tiles rather than two column slots per lane (c5, N = 256: EB
+    // 65.5 -> 62.8 ms, RB 135 -> 100 ms; profiles/r01c_c5_tile_probe.txt).
     (void)h;
-    return 256;
+    return 128;
 }
 
 // DASPMM_EB_CTA=0 disables the CTA-combined EB+SR path (tuning aid).
