@@ -285,6 +285,8 @@ def run_ours(args):
             assembly = _assembly(calls, mats, world, dev)
         except Exception as ex:  # optional measurement: never lose the bench line to it
             assembly = {"error": str(ex)[:200]}
+    if args.roofline_table and rank == 0:
+        _write_roofline_table(args.roofline_table, calls, per_call_ms, chosen, peak)
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
                    flush, assembly)
@@ -461,6 +463,28 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _write_roofline_table(path, calls, per_call_ms, chosen, peak):
+    """Per-call roofline table: algorithmic bytes and their HBM fraction, and the
+    measured ceilings of _ceilings (L2 gather rate, L1 wavefronts); `bound` names the
+    largest ceiling, `frac_bound` = that ceiling's time / the measured time."""
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    lines = ["| call | kernel | us | algorithmic MB | GB/s | frac HBM | hbm us | l2_gather us "
+             "| l1_wavefront us | bound | frac of bound |", "|" + "---|" * 11]
+    for c, t, k in zip(calls, per_call_ms, chosen):
+        ce = _ceilings(c, None, peak)
+        cands = {n: v for n, v in ce.items() if v is not None}
+        bname = max(cands, key=cands.get)
+        us = t * 1e3
+        gbs = c["bytes"] / (t * 1e-3) / 1e9
+        lines.append(f'| {c["m"]["name"]}/N{c["n"]} | {sk.KernelId.from_index(k).name()} | '
+                     f'{us:.1f} | {c["bytes"] / 1e6:.1f} | {gbs:.0f} | {gbs / peak:.3f} | '
+                     f'{ce["hbm"]} | {ce["l2_gather"]} | {ce["l1_wavefront"]} | {bname} | '
+                     f'{cands[bname] / us:.2f} |')
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
 
 
 def _ceilings(c, traffic, peak):
@@ -725,6 +749,8 @@ def main():
     ap.add_argument("--ns", default="")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--roofline-table", default="",
+                    help="also write a per-call roofline table (markdown) to this path")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
