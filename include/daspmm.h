@@ -195,6 +195,11 @@ int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, 
 int daspmm_spmm_rows_to(const daspmm_csr* csr, const void* d_B, int64_t ldb, int64_t N,
                         void* const* d_C, int n_dst, int64_t ldc, daspmm_stream stream);
 
+/* Re-reads the planner's tuning environment variables (DASPMM_LEAN*, DASPMM_EB_*,
+ * DASPMM_RPG, DASPMM_TILE_COLS, DASPMM_WIN, DASPMM_TMA*, fault injection). They are read
+ * once at load; tests and tuning sweeps that change them call this afterwards. */
+int daspmm_reload_env(void);
+
 /* Which launch variant daspmm_spmm would run for these operands (no launch):
  *   variant 0 = the design point's base kernel, 1 = RB+SR with the B window staged in
  *   shared memory (*param = rows per CTA panel), 2 = EB+SR with CTA-combined boundary

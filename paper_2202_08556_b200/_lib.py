@@ -58,6 +58,7 @@ SIGNATURES = {
                                        C.c_uint, _vp, _vp]),
     "daspmm_debug_tree_reduce_f64": (C.c_int, [_vp, _i64, _vp]),
     "daspmm_spmm_rows_to": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _i64, _vp]),
+    "daspmm_reload_env": (C.c_int, []),
     "daspmm_plan_info": (C.c_int, [_vp, C.c_int, _i64, _vp, _i64, _vp, _i64, C.c_uint, _vp, _vp]),
     "daspmm_debug_conditional_scan_f64": (C.c_int, [_vp, _vp, _i64, _vp]),
 }

@@ -97,73 +97,78 @@ static void keep_pool_warm(int dev) {
     done[dev] = true;
 }
 
+// Planner tuning knobs (environment, all optional; documented at their uses and in
+// INTEGRATION.md). Read once into a snapshot so the per-call host path does no getenv;
+// daspmm_reload_env() re-reads them (tests and tuning sweeps that change them).
+struct Knobs {
+    int64_t tile_cols = 0;    // DASPMM_TILE_COLS: column-tile width override
+    bool eb_cta = true;       // DASPMM_EB_CTA=0: no CTA-combined EB+SR walk
+    int64_t eb_chunk = 0;     // DASPMM_EB_CHUNK: EB pairs per group override
+    bool lean = true;         // DASPMM_LEAN=0: no lean SR kernels
+    int lean_min_lanes = 2;   // DASPMM_LEAN_MIN_LANES
+    int64_t lean_chunk = 0;   // DASPMM_LEAN_CHUNK: lean EB chunk override
+    int lean_rw = -1;         // DASPMM_LEAN_RW=0/1: force the segment / range walk
+    bool lean_rb = false;     // DASPMM_LEAN_RB=1: lean walk for RB+SR too
+    int64_t rpg = 0;          // DASPMM_RPG: RB rows per group override
+    int64_t lean_rpg = 0;     // DASPMM_LEAN_RPG
+    bool win = false;         // DASPMM_WIN=1: shared-memory B-window RB kernel
+    bool tma = false;         // DASPMM_TMA=1: TMA gather4 EB kernel
+    int64_t tma_lw = 0;       // DASPMM_TMA_LW: its pairs per warp
+    bool fault = false;       // SPMMKIT_ENABLE_FAULT_INJECTION=1 + DASPMM_INJECT_FAULT=1
+};
+
+static Knobs read_knobs() {
+    auto str = [](const char* n) -> const char* { return getenv(n); };
+    auto i64 = [&](const char* n) { const char* e = str(n); return e ? int64_t(atoll(e)) : int64_t(0); };
+    auto on = [&](const char* n, char v) { const char* e = str(n); return e && e[0] == v; };
+    Knobs k;
+    k.tile_cols = i64("DASPMM_TILE_COLS");
+    k.eb_cta = !on("DASPMM_EB_CTA", '0');
+    k.eb_chunk = i64("DASPMM_EB_CHUNK");
+    k.lean = !on("DASPMM_LEAN", '0');
+    if (str("DASPMM_LEAN_MIN_LANES")) k.lean_min_lanes = int(i64("DASPMM_LEAN_MIN_LANES"));
+    k.lean_chunk = i64("DASPMM_LEAN_CHUNK");
+    if (str("DASPMM_LEAN_RW")) k.lean_rw = on("DASPMM_LEAN_RW", '1') ? 1 : 0;
+    k.lean_rb = on("DASPMM_LEAN_RB", '1');
+    k.rpg = i64("DASPMM_RPG");
+    k.lean_rpg = i64("DASPMM_LEAN_RPG");
+    k.win = on("DASPMM_WIN", '1');
+    k.tma = on("DASPMM_TMA", '1');
+    k.tma_lw = i64("DASPMM_TMA_LW");
+    k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
+    return k;
+}
+
+static std::mutex g_knobs_mu;
+static Knobs g_knobs = read_knobs();
+
+static Knobs knobs() {
+    std::lock_guard<std::mutex> lk(g_knobs_mu);
+    return g_knobs;
+}
+
 // Column-tile width: B's working set for one tile of columns, K x tile x elem, should
 // stay L2-resident (126 MB on B200) while A streams through. CTAs are scheduled
-// x-major, so tiles (blockIdx.y) run one after another. DASPMM_TILE_COLS overrides.
-static int64_t max_tile_cols(const daspmm_csr* h, int64_t N) {
-    static const int64_t env = [] {
-        const char* e = getenv("DASPMM_TILE_COLS");
-        return e ? int64_t(atoll(e)) : int64_t(0);
-    }();
-    if (env > 0) return env;
+// x-major, so tiles (blockIdx.y) run one after another.
+static int64_t max_tile_cols(const Knobs& kn) {
+    if (kn.tile_cols > 0) return kn.tile_cols;
     // Measured on B200 (profiles/r01_notes.md): narrowing tiles to keep B in L2 costs
     // more in A re-reads and shorter gathers than it saves, up to N = 128. Wider N runs
     // 128-column y-tiles rather than two column slots per lane (c5, N = 256: EB
     // 65.5 -> 62.8 ms, RB 135 -> 100 ms; profiles/r01c_c5_tile_probe.txt).
-    (void)h;
     return 128;
 }
 
-// DASPMM_EB_CTA=0 disables the CTA-combined EB+SR path (tuning aid).
-static bool eb_cta_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("DASPMM_EB_CTA");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-// EB chunk count for a chunk length; DASPMM_EB_CHUNK overrides the length (tuning aid).
-static int64_t auto_chunks(int64_t nnz, int64_t chunk) {
+// EB chunk count for a chunk length (DASPMM_EB_CHUNK overrides the length).
+static int64_t auto_chunks(const Knobs& kn, int64_t nnz, int64_t chunk) {
     if (nnz <= 0) return 1;
-    static const int64_t env = [] {
-        const char* e = getenv("DASPMM_EB_CHUNK");
-        return e ? int64_t(atoll(e)) : int64_t(0);
-    }();
-    if (env > 0) chunk = env;
+    if (kn.eb_chunk > 0) chunk = kn.eb_chunk;
     return (nnz + chunk - 1) / chunk;
 }
 
-// DASPMM_LEAN=0 disables the lean SR kernels; DASPMM_LEAN_MIN_LANES (default 2) is the
-// narrowest lane group they take; DASPMM_LEAN_CHUNK the EB chunk (tuning aids).
-static bool lean_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("DASPMM_LEAN");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-static int lean_min_lanes() {
-    static const int v = [] {
-        const char* e = getenv("DASPMM_LEAN_MIN_LANES");
-        return e ? atoi(e) : 2;
-    }();
-    return v;
-}
-static int64_t lean_chunk(bool range_walk) {
-    static const int64_t env = [] {
-        const char* e = getenv("DASPMM_LEAN_CHUNK");
-        return e ? int64_t(atoll(e)) : int64_t(0);
-    }();
+static int64_t lean_chunk(const Knobs& kn, bool range_walk) {
     // measured: 128 pairs for the range walk, 256 for the segment walk (c3 4.47 -> 4.34 ms)
-    return env > 0 ? env : (range_walk ? 128 : 256);
-}
-
-// DASPMM_WIN=1 enables the RB+SR B-window kernel (opt-in: on B200 the L1 already
-// serves row-local gathers, measured no gain; kept as a tuning aid).
-static bool win_enabled() {  // read per plan so tests can toggle it
-    const char* e = getenv("DASPMM_WIN");
-    return e && e[0] == '1';
+    return kn.lean_chunk > 0 ? kn.lean_chunk : (range_walk ? 128 : 256);
 }
 
 // RB+RM+SR on row-local matrices: stage each CTA panel's B window in shared memory
@@ -171,9 +176,9 @@ static bool win_enabled() {  // read per plan so tests can toggle it
 // reused by several nonzeros. The panel height is the largest R = 32 << i that still
 // gives >= 2 CTAs per SM; the staging must fit kWinSmemMax for the widest panel.
 static void plan_window(const daspmm_csr* h, Plan& p, int64_t N, int64_t tile_cols,
-                        int64_t ytiles, const void* B, bool exact) {
+                        int64_t ytiles, const void* B, bool exact, bool enabled) {
     p.win_rows = 0;
-    if (exact || p.cm || h->dtype != DASPMM_F32 || !win_enabled() || h->spans == nullptr ||
+    if (exact || p.cm || h->dtype != DASPMM_F32 || !enabled || h->spans == nullptr ||
         h->M <= 0 || h->nnz <= 0 || B == nullptr)
         return;
     const int64_t pitch = std::min<int64_t>(N, tile_cols);
@@ -192,15 +197,9 @@ static void plan_window(const daspmm_csr* h, Plan& p, int64_t N, int64_t tile_co
 }
 
 // Self-test fault hook (the reference's `validate --inject-fault`, spmmkit_cli.cpp:
-// 366-371, 394-397): with SPMMKIT_ENABLE_FAULT_INJECTION=1 and DASPMM_INJECT_FAULT=1 every
-// device SpMM adds 1 to C[0][0], so tests can prove the parity checks catch a wrong
-// result. Read per call; never set in normal use.
-static bool fault_injection_armed() {
-    const char* en = getenv("SPMMKIT_ENABLE_FAULT_INJECTION");
-    const char* f = getenv("DASPMM_INJECT_FAULT");
-    return en && en[0] == '1' && f && f[0] == '1';
-}
-
+// 366-371, 394-397): with SPMMKIT_ENABLE_FAULT_INJECTION=1 and DASPMM_INJECT_FAULT=1
+// (Knobs::fault) every device SpMM adds 1 to C[0][0], so tests can prove the parity
+// checks catch a wrong result. Never set in normal use.
 template <typename T>
 __global__ void k_inject_fault(T* c) {
     c[0] += T(1);
@@ -214,6 +213,7 @@ static cudaError_t inject_fault(int dtype, void* C, cudaStream_t s) {
 
 Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N, const void* B,
                int64_t ldb, const void* C, int64_t ldc, bool exact, bool base_only) {
+    const Knobs kn = knobs();
     Plan p;
     p.kernel = kernel;
     p.cm = (kernel >> 1) & 1;
@@ -232,7 +232,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             p.V /= 2;
         }
     }
-    const int64_t ncols = std::min<int64_t>(N, max_tile_cols(h, N));
+    const int64_t ncols = std::min<int64_t>(N, max_tile_cols(kn));
     const int64_t nv = (ncols + p.V - 1) / p.V;  // column slots per tile
     int64_t tile_cols;
     int lanes;
@@ -250,8 +250,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     // Lean SR kernels (lean.cuh): fp32 fast mode, row-major B, groups of >= 2 lanes,
     // quad-aligned A arrays. One column slot per lane; wider N takes more y-tiles.
     p.lean = !base_only && !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 &&
-             lean_enabled() &&
-             p.L >= lean_min_lanes() && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
+             kn.lean &&
+             p.L >= kn.lean_min_lanes && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
              (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
                                            reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
     // Where the lean walks win (measured on B200 against the shuffle-broadcast walks with
@@ -265,10 +265,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     const double avg_nonempty =
         h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty) : 0.0;
     const bool lean_ok = p.lean;  // eligibility (also of the TMA-gather variant)
-    if (p.lean && !eb) {
-        const char* e = getenv("DASPMM_LEAN_RB");
-        p.lean = e && e[0] == '1';
-    }
+    if (p.lean && !eb) p.lean = kn.lean_rb;
     if (p.lean && eb && N > 16 && avg_nonempty < 48.0) p.lean = false;
     if (p.lean) {
         p.X = 1;
@@ -277,14 +274,13 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     const int64_t ytiles = std::max<int64_t>(1, (N + tile_cols - 1) / tile_cols);
     int64_t workers;
     // TMA gather4 EB kernel (opt-in while being measured: DASPMM_TMA=1)
-    if (eb && lean_ok && N >= 32 && getenv("DASPMM_TMA") && getenv("DASPMM_TMA")[0] == '1' &&
+    if (eb && lean_ok && N >= 32 && kn.tma &&
         tma_gather_supported(B, ldb, N, h->K) && h->nnz < (int64_t(1) << 31) - 1024) {
         p.tma = true;
         p.lean = false;
         const int bc = tma_box_cols(N);
         p.sub = 256;  // Lw: nonzeros per warp (multiple of 16)
-        const char* lw = getenv("DASPMM_TMA_LW");
-        if (lw && atoi(lw) >= 16) p.sub = (atoi(lw) / 16) * 16;
+        if (kn.tma_lw >= 16) p.sub = (kn.tma_lw / 16) * 16;
         p.P = (h->nnz + p.sub - 1) / p.sub;  // warps
         p.grid = dim3(unsigned((p.P + kTmaWarpsHost - 1) / kTmaWarpsHost),
                       unsigned((N + bc - 1) / bc), 1);
@@ -293,15 +289,14 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     if (eb && p.lean) {
         // short rows: range walk (COO ids per block); long rows: segment walk.
         // DASPMM_LEAN_RW=0/1 forces one (tuning aid).
-        const char* rw = getenv("DASPMM_LEAN_RW");
         // Measured on B200: the range walk wins on short rows (power-law s20 N = 16:
         // 342 -> 217 us), the segment walk on long rows (c3: 5.26 -> 4.07 ms).
-        p.lean_rw = rw ? rw[0] == '1' : avg_nonempty < 48.0;
-        p.sub = lean_chunk(p.lean_rw);
+        p.lean_rw = kn.lean_rw >= 0 ? kn.lean_rw == 1 : avg_nonempty < 48.0;
+        p.sub = lean_chunk(kn, p.lean_rw);
         // small matrices: shorten chunks until there are >= 4 CTAs per SM (s14 power-law,
         // N = 128: 128 CTAs at 256 pairs -> 88 us, vs 32 us with the grid filled)
         const int64_t fill = h->nnz * p.L / (148LL * 4 * kThreads);
-        if (!getenv("DASPMM_LEAN_CHUNK") && fill < p.sub) p.sub = std::max<int64_t>(32, fill & ~7LL);
+        if (kn.lean_chunk <= 0 && fill < p.sub) p.sub = std::max<int64_t>(32, fill & ~7LL);
         p.P = (h->nnz + p.sub - 1) / p.sub;
         workers = std::max<int64_t>(p.P, 1);
     } else if (eb) {
@@ -315,7 +310,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             const int64_t fill = h->nnz * p.L / (148LL * (p.L >= 32 ? 4 : 8) * kThreads);
             chunk = int(std::max<int64_t>(chunk, std::min<int64_t>(256, fill)));
         }
-        p.P = P > 0 ? P : auto_chunks(h->nnz, chunk);
+        p.P = P > 0 ? P : auto_chunks(kn, h->nnz, chunk);
         workers = p.P;
         if (!pr && !exact && P <= 0 && p.L == 1 && p.X == 1 && N <= p.V && !p.cm &&
             h->dtype == DASPMM_F32) {
@@ -324,7 +319,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             p.sub = p.V >= 4 ? kThrS4 : kThrS;  // 3 x sub x 256 x 4 B of staging < 48 KB
             p.P = (h->nnz + p.sub - 1) / p.sub;
             workers = p.P;
-        } else if (!pr && !exact && P <= 0 && eb_cta_enabled()) {  // CTA-combined boundary rows
+        } else if (!pr && !exact && P <= 0 && kn.eb_cta) {  // CTA-combined boundary rows
             p.cta = true;
             p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
             p.sub = std::max<int64_t>(p.sub, 1);
@@ -342,21 +337,11 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         if (sd > 2.0 * avg) rpg = 1;
         const int64_t cap = std::max<int64_t>(1, h->M * lanes / (2LL * 148 * 2048));
         rpg = std::max<int64_t>(1, std::min<int64_t>({rpg, cap, int64_t(p.L)}));  // <= LPR
-        static const int64_t env_rpg = [] {
-            const char* e = getenv("DASPMM_RPG");
-            return e ? int64_t(atoll(e)) : int64_t(0);
-        }();
-        if (env_rpg > 0) rpg = std::min<int64_t>(env_rpg, p.L);
-        if (p.lean) {
-            static const int64_t env_lrpg = [] {
-                const char* e = getenv("DASPMM_LEAN_RPG");
-                return e ? int64_t(atoll(e)) : int64_t(0);
-            }();
-            if (env_lrpg > 0) rpg = env_lrpg;
-        }
+        if (kn.rpg > 0) rpg = std::min<int64_t>(kn.rpg, p.L);
+        if (p.lean && kn.lean_rpg > 0) rpg = kn.lean_rpg;
         p.rpg = rpg;
         workers = (h->M + rpg - 1) / rpg;
-        if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact);
+        if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact, kn.win);
         if (p.win_rows > 0) {
             p.lean = false;
             p.grid = dim3(unsigned((h->M + p.win_rows - 1) / p.win_rows), unsigned(ytiles), 1);
@@ -460,7 +445,7 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     e = h->dtype == DASPMM_F64 ? run_plan<double>(h, p, W, B, ldb, N, C, ldc, chunk_row, s)
                                : run_plan<float>(h, p, W, B, ldb, N, C, ldc, chunk_row, s);
     if (chunk_row && own_scratch) cudaFreeAsync(chunk_row, s);
-    if (e == cudaSuccess && fault_injection_armed()) e = inject_fault(h->dtype, C, s);
+    if (e == cudaSuccess && knobs().fault) e = inject_fault(h->dtype, C, s);
     if (e == cudaErrorNotSupported)
         return fail(DASPMM_ERR_UNSUPPORTED, std::string("spmm: no instantiation for kernel ") +
                                                 kKernelNames[kernel]);
@@ -865,6 +850,13 @@ int daspmm_partition(const daspmm_csr* h, int64_t p, int64_t* begin, int64_t* en
         if (row) row[i] = rows[size_t(i)];
         start += size;
     }
+    return DASPMM_OK;
+}
+
+int daspmm_reload_env(void) {
+    const Knobs k = read_knobs();
+    std::lock_guard<std::mutex> lk(g_knobs_mu);
+    g_knobs = k;
     return DASPMM_OK;
 }
 

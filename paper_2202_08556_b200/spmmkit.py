@@ -392,6 +392,11 @@ def spmm_rows_to(a: DeviceCsr, B, outs, stream=None):
     return outs[0]
 
 
+def reload_env():
+    """Re-read the planner's tuning environment variables (daspmm_reload_env)."""
+    check(lib().daspmm_reload_env())
+
+
 PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma"}
 
 

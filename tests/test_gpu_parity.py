@@ -440,7 +440,8 @@ def test_rb_window_kernel_banded(sk, b):
 
     a = _banded_csr(6000, b, seed=b, empty_every=7)
     d = sk.DeviceCsr.from_host(a)
-    os.environ["DASPMM_WIN"] = "1"  # opt-in kernel (plan reads it per call)
+    os.environ["DASPMM_WIN"] = "1"  # opt-in kernel
+    sk.reload_env()
     bound_cache = {}
     variants = set()
     for n in (1, 2, 3, 4, 8, 16, 32, 33, 64, 100, 128, 256, 300):
@@ -465,6 +466,7 @@ def test_rb_window_kernel_banded(sk, b):
             err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
             assert (err <= bound).all(), f"b{b} n{n} {mode} ({variant}, {rows}): {err.max()}"
     del os.environ["DASPMM_WIN"]
+    sk.reload_env()
     assert "rb_window" in variants
 
 
@@ -478,10 +480,12 @@ def test_rb_window_not_used_on_scattered_columns(sk):
     B = torch.zeros(4000, 32, device="cuda")
     C = torch.zeros(4000, 32, device="cuda")
     os.environ["DASPMM_WIN"] = "1"
+    sk.reload_env()
     try:
         assert sk.plan_info(0, d, B, C)[0] != "rb_window"
     finally:
         del os.environ["DASPMM_WIN"]
+        sk.reload_env()
 
 
 @pytest.mark.parametrize("kernel", [0, 4])
@@ -497,7 +501,8 @@ def test_lean_sr_kernels(sk, kernel, skew):
     a = H.random_csr(5003, 4001, 90001, seed=11 + kernel, dtype=np.float32, skew=skew)
     d = sk.DeviceCsr.from_host(a)
     seen = set()
-    os.environ["DASPMM_LEAN_RB"] = "1"  # RB lean walk is opt-in (plan reads it per call)
+    os.environ["DASPMM_LEAN_RB"] = "1"  # RB lean walk is opt-in
+    sk.reload_env()
     for n in (8, 16, 24, 32, 64, 96, 128, 200, 256):
         x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
         y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
@@ -515,6 +520,7 @@ def test_lean_sr_kernels(sk, kernel, skew):
             err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
             assert (err <= bound).all(), f"k{kernel} n{n} padded={padded}: {np.nanmax(err)}"
     del os.environ["DASPMM_LEAN_RB"]
+    sk.reload_env()
     assert "lean" in seen
 
 
@@ -530,6 +536,7 @@ def test_eb_tma_gather_kernel(sk, skew):
     a = H.random_csr(5003, 4001, 90001, seed=21, dtype=np.float32, skew=skew)
     d = sk.DeviceCsr.from_host(a)
     os.environ["DASPMM_TMA"] = "1"
+    sk.reload_env()
     try:
         for n in (32, 40, 64, 100, 128, 256, 300):
             x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
@@ -549,6 +556,7 @@ def test_eb_tma_gather_kernel(sk, skew):
                 assert (err <= bound).all(), f"n{n} padded={padded}: {np.nanmax(err)}"
     finally:
         del os.environ["DASPMM_TMA"]
+        sk.reload_env()
 
 
 def test_gcn_layer_matches_dense_reference(sk):
@@ -676,8 +684,10 @@ def test_fault_injection_is_caught(sk):
     assert run()
     os.environ["SPMMKIT_ENABLE_FAULT_INJECTION"] = "1"
     os.environ["DASPMM_INJECT_FAULT"] = "1"
+    sk.reload_env()
     try:
         assert not run()
     finally:
         del os.environ["SPMMKIT_ENABLE_FAULT_INJECTION"], os.environ["DASPMM_INJECT_FAULT"]
+        sk.reload_env()
     assert run()

@@ -33,6 +33,7 @@ for dtype in (np.float32, np.float64):
             sk.spmm_selected(d, model, B, C, kernel_out=kout)
 # opt-in launch variants: lean RB walk, TMA gather4 EB kernel, shared-memory B window
 os.environ["DASPMM_LEAN_RB"] = "1"
+sk.reload_env()
 a = H.random_csr(700, 600, 9000, seed=4, dtype=np.float32, skew=1.4)
 d = sk.DeviceCsr.from_host(a)
 for n in (8, 16, 33, 128):
@@ -40,14 +41,17 @@ for n in (8, 16, 33, 128):
     C = torch.empty(700, n, device="cuda")
     sk.spmm_device(0, d, B, C)
 del os.environ["DASPMM_LEAN_RB"]
+sk.reload_env()
 a = H.random_csr(700, 600, 9001, seed=5, dtype=np.float32, skew=1.2)
 d = sk.DeviceCsr.from_host(a)
 os.environ["DASPMM_TMA"] = "1"
+sk.reload_env()
 for n in (32, 64, 100, 128):
     B = torch.rand(600, n, device="cuda")
     C = torch.empty(700, n, device="cuda")
     sk.spmm_device(4, d, B, C)
 del os.environ["DASPMM_TMA"]
+sk.reload_env()
 rows = np.repeat(np.arange(2000), 9)
 cols = rows + np.tile(np.arange(-4, 5), 2000)
 keep = (cols >= 0) & (cols < 2000)
@@ -57,11 +61,13 @@ band = sk.CsrMatrix(2000, 2000, rp, cols[keep].astype(np.int64),
                     np.float32)
 d = sk.DeviceCsr.from_host(band)
 os.environ["DASPMM_WIN"] = "1"
+sk.reload_env()
 for n in (2, 8, 32, 128):
     B = torch.rand(2000, n, device="cuda")
     C = torch.empty(2000, n, device="cuda")
     sk.spmm_device(0, d, B, C)
 del os.environ["DASPMM_WIN"]
+sk.reload_env()
 # replicated RB+RM+SR epilogue (fused row-panel SpMM + all-gather), three destinations
 for n in (3, 32, 128):
     B = torch.rand(2000, n, device="cuda")
