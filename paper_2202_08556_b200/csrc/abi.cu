@@ -115,6 +115,10 @@ struct Knobs {
     bool tma = false;         // DASPMM_TMA=1: TMA gather4 EB kernel
     int64_t tma_lw = 0;       // DASPMM_TMA_LW: its pairs per warp
     bool fault = false;       // SPMMKIT_ENABLE_FAULT_INJECTION=1 + DASPMM_INJECT_FAULT=1
+    // DASPMM_CTA_THREADS (64/128/256): CTA size of the CTA-combined EB walk. Measured:
+    // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
+    // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
+    int cta_threads = 64;
 };
 
 static Knobs read_knobs() {
@@ -136,6 +140,8 @@ static Knobs read_knobs() {
     k.tma = on("DASPMM_TMA", '1');
     k.tma_lw = i64("DASPMM_TMA_LW");
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
+    if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 64 || t == 128 || t == 256)
+        k.cta_threads = int(t);
     return k;
 }
 
@@ -321,6 +327,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             workers = p.P;
         } else if (!pr && !exact && P <= 0 && kn.eb_cta) {  // CTA-combined boundary rows
             p.cta = true;
+            p.cta_threads = kn.cta_threads;
             p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
             p.sub = std::max<int64_t>(p.sub, 1);
             p.P = (h->nnz + p.sub - 1) / p.sub;
@@ -351,8 +358,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         workers = h->M;
     }
     const int64_t threads = workers * lanes;
-    p.grid = dim3(unsigned(std::max<int64_t>(1, (threads + kThreads - 1) / kThreads)),
-                  unsigned(ytiles), 1);
+    const int64_t cta = p.cta ? p.cta_threads : kThreads;
+    p.grid = dim3(unsigned(std::max<int64_t>(1, (threads + cta - 1) / cta)), unsigned(ytiles), 1);
     return p;
 }
 
@@ -408,7 +415,7 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
         cudaError_t e =
             (p.cta || p.thr)
                   ? launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P,
-                                              p.thr ? 32 : kThreads / p.L,
+                                              p.thr ? 32 : p.cta_threads / p.L,
                                               static_cast<T*>(C), ldc, int(N), h->empty_rows,
                                               int(h->n_empty), s)
                   : launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,

@@ -21,6 +21,7 @@ struct Plan {
     int64_t P = 0;       // EB chunks
     int64_t rpg = 1;     // RB+SR rows per group (row-block size)
     bool cta = false;    // EB+SR fast path: CTA-combined boundary rows (k_eb_sr_cta)
+    int cta_threads = 64;   // ... its CTA size (64, 128 or 256)
     bool thr = false;    // EB+SR fast path for one-lane groups: staged sub-chunks (k_eb_sr_thr)
     int64_t sub = 0;     // ... its pairs per group sub-chunk
     bool lean = false;   // RB/EB+RM+SR lean kernels (lean.cuh), fp32 fast mode

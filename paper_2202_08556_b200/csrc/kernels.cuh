@@ -430,18 +430,18 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
 // shared memory and stored once; only rows crossing the CTA's own range take an
 // atomic (pre-zeroed by k_eb_prep_uniform). Long power-law rows thus receive one
 // atomic per CTA instead of one per group.
-template <typename T, bool CM, int V, int LPR, int CPL>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4)
+template <typename T, bool CM, int V, int LPR, int CPL, int NT = kThreads>
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 8 || LPR <= 2) ? 3 : 4) * (kThreads / NT))
 k_eb_sr_cta(const SpmmArgs<T> a) {
-    constexpr int G = kThreads / LPR;
+    constexpr int G = NT / LPR;
     constexpr int TN = LPR * V * CPL;
     // +1 padding: ptxas pairs the combine loop's loads into 64-bit LDS, and with an odd
     // trip count (G + 1) the last pair would read one element past the array.
     __shared__ T sL[(G + 2) * TN];
     __shared__ T sR[(G + 2) * TN];
     __shared__ int srow[G + 2];
-    for (int i = threadIdx.x; i < (G + 2) * TN; i += kThreads) sL[i] = sR[i] = T(0);
-    for (int i = threadIdx.x; i < G + 2; i += kThreads) srow[i] = -1;
+    for (int i = threadIdx.x; i < (G + 2) * TN; i += NT) sL[i] = sR[i] = T(0);
+    for (int i = threadIdx.x; i < G + 2; i += NT) srow[i] = -1;
     __syncthreads();
 
     const unsigned mask = group_mask<LPR>();
@@ -459,7 +459,7 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
                                                    mask, gl, slots);
     __syncthreads();
     // Combine: thread t owns tile column t; boundaries in order, segmented by row.
-    for (int t = threadIdx.x; t < TN; t += kThreads) {
+    for (int t = threadIdx.x; t < TN; t += NT) {
         const int col = tile0 + t;
         if (col >= a.N) continue;
         int cur = -1;

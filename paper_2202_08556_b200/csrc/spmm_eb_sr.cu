@@ -3,19 +3,23 @@
 namespace daspmm {
 // Fast path instantiations (CTA-combined boundary rows); the exact path keeps one
 // partition chunk per group (k_eb_sr) so owned rows match the reference bit for bit.
-#define DASPMM_CTA_LPR_TABLE(T, CM, V)                                                      \
+#define DASPMM_CTA_LPR_TABLE_NT(T, CM, V, NT)                                             \
     switch (p.L) {                                                                        \
-        case 1: k_eb_sr_cta<T, CM, V, 1, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
-        case 2: k_eb_sr_cta<T, CM, V, 2, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
-        case 4: k_eb_sr_cta<T, CM, V, 4, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
-        case 8: k_eb_sr_cta<T, CM, V, 8, 1><<<p.grid, kThreads, 0, s>>>(a); break;        \
-        case 16: k_eb_sr_cta<T, CM, V, 16, 1><<<p.grid, kThreads, 0, s>>>(a); break;      \
+        case 1: k_eb_sr_cta<T, CM, V, 1, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
+        case 2: k_eb_sr_cta<T, CM, V, 2, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
+        case 4: k_eb_sr_cta<T, CM, V, 4, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
+        case 8: k_eb_sr_cta<T, CM, V, 8, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
+        case 16: k_eb_sr_cta<T, CM, V, 16, 1, NT><<<p.grid, NT, 0, s>>>(a); break;        \
         case 32:                                                                          \
-            if (p.X == 2) k_eb_sr_cta<T, CM, V, 32, 2><<<p.grid, kThreads, 0, s>>>(a);    \
-            else k_eb_sr_cta<T, CM, V, 32, 1><<<p.grid, kThreads, 0, s>>>(a);             \
+            if (p.X == 2) k_eb_sr_cta<T, CM, V, 32, 2, NT><<<p.grid, NT, 0, s>>>(a);      \
+            else k_eb_sr_cta<T, CM, V, 32, 1, NT><<<p.grid, NT, 0, s>>>(a);               \
             break;                                                                        \
         default: return cudaErrorNotSupported;                                            \
     }
+#define DASPMM_CTA_LPR_TABLE(T, CM, V)                                                    \
+    if (p.cta_threads == 64) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 64) }                    \
+    else if (p.cta_threads == 128) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 128) }             \
+    else { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, kThreads) }
 
 template <typename T>
 static cudaError_t launch_eb_sr_cta(const Plan& p, const SpmmArgs<T>& a, cudaStream_t s) {
