@@ -119,6 +119,15 @@ struct Knobs {
     // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
     // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
     int cta_threads = 64;
+    // DASPMM_THR_THREADS (64/128/256): CTA size of the one-lane staged path (measured:
+    // 64 -> uniform s20 N = 4 121 -> 105 us, N = 2 105 -> 97; r01c_thr_threads_probe.txt).
+    int thr_threads = 64;
+    // DASPMM_RB_THREADS (64/128/256): CTA size of fast RB+RM+SR (measured: 128 -> banded
+    // s20 N = 8 90 -> 82 us, uniform s20 N = 8 133 -> 123; r01c_rb_threads_probe.txt).
+    int rb_threads = 128;
+    // DASPMM_LEAN_THREADS (128/256): CTA size of the lean kernels (measured: 128 -> c3
+    // 3.78 -> 3.69 ms, power-law s20 N = 8 174 -> 156 us; r01c_lean_threads_probe.txt).
+    int lean_threads = 128;
 };
 
 static Knobs read_knobs() {
@@ -142,6 +151,12 @@ static Knobs read_knobs() {
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
     if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 64 || t == 128 || t == 256)
         k.cta_threads = int(t);
+    if (const int64_t t = i64("DASPMM_THR_THREADS"); t == 64 || t == 128 || t == 256)
+        k.thr_threads = int(t);
+    if (const int64_t t = i64("DASPMM_RB_THREADS"); t == 64 || t == 128 || t == 256)
+        k.rb_threads = int(t);
+    if (const int64_t t = i64("DASPMM_LEAN_THREADS"); t == 128 || t == 256)
+        k.lean_threads = int(t);
     return k;
 }
 
@@ -322,6 +337,7 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             h->dtype == DASPMM_F32) {
             // one-lane groups: CTA-staged thread sub-chunks (k_eb_sr_thr)
             p.thr = true;
+            p.thr_threads = kn.thr_threads;
             p.sub = p.V >= 4 ? kThrS4 : kThrS;  // 3 x sub x 256 x 4 B of staging < 48 KB
             p.P = (h->nnz + p.sub - 1) / p.sub;
             workers = p.P;
@@ -347,6 +363,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         if (kn.rpg > 0) rpg = std::min<int64_t>(kn.rpg, p.L);
         if (p.lean && kn.lean_rpg > 0) rpg = kn.lean_rpg;
         p.rpg = rpg;
+        if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && !p.lean)
+            p.rb_threads = kn.rb_threads;
         workers = (h->M + rpg - 1) / rpg;
         if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact, kn.win);
         if (p.win_rows > 0) {
@@ -358,7 +376,10 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         workers = h->M;
     }
     const int64_t threads = workers * lanes;
-    const int64_t cta = p.cta ? p.cta_threads : kThreads;
+    if (p.lean) p.lean_threads = kn.lean_threads;
+    const int64_t cta = p.cta ? p.cta_threads : p.thr ? p.thr_threads
+                      : p.lean ? p.lean_threads
+                      : (!eb && !pr && p.win_rows == 0) ? p.rb_threads : kThreads;
     p.grid = dim3(unsigned(std::max<int64_t>(1, (threads + cta - 1) / cta)), unsigned(ytiles), 1);
     return p;
 }

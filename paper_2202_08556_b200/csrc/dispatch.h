@@ -24,6 +24,9 @@ struct Plan {
     int cta_threads = 64;   // ... its CTA size (64, 128 or 256)
     bool thr = false;    // EB+SR fast path for one-lane groups: staged sub-chunks (k_eb_sr_thr)
     int64_t sub = 0;     // ... its pairs per group sub-chunk
+    int thr_threads = 256;  // CTA size of the one-lane staged path (64, 128 or 256)
+    int rb_threads = 256;   // CTA size of fast f32 RB+RM+SR (k_rb_sr)
+    int lean_threads = 256; // CTA size of the lean kernels (128 or 256)
     bool lean = false;   // RB/EB+RM+SR lean kernels (lean.cuh), fp32 fast mode
     bool lean_rw = false;  // ... EB: range walk with COO row ids (short rows)
     bool tma = false;    // EB+RM+SR with TMA gather4 B-row fetches (tma_gather.cuh)

@@ -312,13 +312,13 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
 // Resident CTAs per SM (measured, profiles/r01c_minblocks_probe.txt): 5 for groups of
 // >= 16 lanes (48 registers; uniform s20 N = 128 1229 -> 1210 us), 4 below (5 costs
 // N = 16 184 -> 221 us), 3 for narrow groups and fp64.
-template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE = kRB>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : (LPR >= 16 ? 5 : 4))
+template <typename T, bool CM, bool EXACT, int V, int LPR, int CPL, int MODE = kRB, int NT = kThreads>
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 8 || LPR <= 2) ? 3 : (LPR >= 16 ? 5 : 4)) * (kThreads / NT))
 k_rb_sr(const SpmmArgs<T> a) {
     constexpr int TN = LPR * V * CPL;
     const unsigned mask = group_mask<LPR>();
     const int gl = threadIdx.x & (LPR - 1);
-    const int64_t g = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    const int64_t g = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t r0 = g * a.rpg;
     if (r0 >= a.M) return;  // whole group leaves together
     const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
@@ -492,23 +492,23 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
 // reads); each thread then issues all S of its B gathers before accumulating, so a
 // warp keeps 32*S gathers in flight. Owned rows are stored, rows cut by a sub-chunk
 // boundary take atomics (pre-zeroed by k_eb_prep_uniform with G = 1).
-template <typename T, bool CM, int V, int S>
-__global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) {
+template <typename T, bool CM, int V, int S, int NT = kThreads>
+__global__ void __launch_bounds__(NT, 3 * (kThreads / NT)) k_eb_sr_thr(const SpmmArgs<T> a) {
     // Per-thread reads of the staged tile are conflict-free for odd S (scalar) and for
     // S = 4 x odd (128-bit reads: 8 lanes per phase hit 8 distinct 16-B bank groups).
     static_assert(S % 2 == 1 || (S % 4 == 0 && (S / 4) % 2 == 1), "conflict-free S");
-    static_assert((kThreads * S * sizeof(int)) % 16 == 0, "TMA bulk size granularity");
+    static_assert((NT * S * sizeof(int)) % 16 == 0, "TMA bulk size granularity");
     // natural order: pair i of thread t at [t*S + i]
-    __shared__ __align__(16) int s_c[S * kThreads];
-    __shared__ __align__(16) int s_r[S * kThreads];
-    __shared__ __align__(16) T s_v[S * kThreads];
+    __shared__ __align__(16) int s_c[S * NT];
+    __shared__ __align__(16) int s_r[S * NT];
+    __shared__ __align__(16) T s_v[S * NT];
     __shared__ uint64_t bar;
-    const int64_t E0 = int64_t(blockIdx.x) * kThreads * S;
-    const int64_t E1 = min(a.nnz, E0 + int64_t(kThreads) * S);
-    if (a.bulk_ok && E1 - E0 == int64_t(kThreads) * S) {
+    const int64_t E0 = int64_t(blockIdx.x) * NT * S;
+    const int64_t E1 = min(a.nnz, E0 + int64_t(NT) * S);
+    if (a.bulk_ok && E1 - E0 == int64_t(NT) * S) {
         // Full tile: three 1-D TMA bulk copies, one elected thread, mbarrier completion.
-        constexpr unsigned kIdxBytes = kThreads * S * sizeof(int);
-        constexpr unsigned kValBytes = kThreads * S * sizeof(T);
+        constexpr unsigned kIdxBytes = NT * S * sizeof(int);
+        constexpr unsigned kValBytes = NT * S * sizeof(T);
         if (threadIdx.x == 0) mbar_init(&bar, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
         T lv[S];
 #pragma unroll
         for (int k = 0; k < S; ++k) {
-            const int64_t e = E0 + k * kThreads + threadIdx.x;
+            const int64_t e = E0 + k * NT + threadIdx.x;
             const bool ok = e < E1;
             lc[k] = ok ? ld_stream(a.ci + e) : 0;
             lv[k] = ok ? ld_stream(a.va + e) : T(0);
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_eb_sr_thr(const SpmmArgs<T> a) 
         }
 #pragma unroll
         for (int k = 0; k < S; ++k) {
-            const int jj = k * kThreads + threadIdx.x;
+            const int jj = k * NT + threadIdx.x;
             s_c[jj] = lc[k];
             s_v[jj] = lv[k];
             s_r[jj] = lr[k];

@@ -204,10 +204,10 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
 
 // RB: group g owns rows [g*rpg, (g+1)*rpg), one row segment at a time; every row is
 // owned (plain stores; empty rows store zeros).
-template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, kLeanMinBlocksRB) k_rb_sr_lean(const SpmmArgs<float> a) {
+template <int V, int LPR, int NT = kThreads>
+__global__ void __launch_bounds__(NT, kLeanMinBlocksRB * (kThreads / NT)) k_rb_sr_lean(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
-    const int64_t g = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    const int64_t g = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t r0 = g * a.rpg;
     if (r0 >= a.M) return;
     const int r1 = int(min(int64_t(a.M), r0 + a.rpg));
@@ -227,10 +227,10 @@ __global__ void __launch_bounds__(kThreads, kLeanMinBlocksRB) k_rb_sr_lean(const
 // EB, segment walk: group w owns the nnz chunk [w*sub, (w+1)*sub) and walks it one row
 // segment at a time (next row from the COO id of the segment's end, so empty rows cost
 // nothing). Rows cut by the chunk ends take atomics. Suits long rows.
-template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, kLeanMinBlocksEB) k_eb_sr_lean(const SpmmArgs<float> a) {
+template <int V, int LPR, int NT = kThreads>
+__global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_sr_lean(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
-    const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
     if (e0l >= a.nnz) return;
     const int e0 = int(e0l), e1 = int(min(a.nnz, e0l + a.sub));
@@ -258,10 +258,10 @@ __global__ void __launch_bounds__(kThreads, kLeanMinBlocksEB) k_eb_sr_lean(const
 
 // EB, range walk: the chunk as one nonzero range with COO row ids (range_walk). Suits
 // short rows (power-law tails), where per-segment row-offset lookups would dominate.
-template <int V, int LPR>
-__global__ void __launch_bounds__(kThreads, kLeanMinBlocksEB) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
+template <int V, int LPR, int NT = kThreads>
+__global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
-    const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
+    const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
     if (e0l >= a.nnz) return;
     const int e0 = int(e0l), e1 = int(min(a.nnz, e0l + a.sub));

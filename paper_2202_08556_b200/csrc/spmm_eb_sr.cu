@@ -45,14 +45,21 @@ cudaError_t launch_eb_sr_per_chunk(const Plan&, const SpmmArgs<T>&, cudaStream_t
 DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
 #undef launch_eb_sr
 
-static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+template <int NT>
+static cudaError_t launch_eb_sr_thr_nt(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
     switch (p.V) {
-        case 1: k_eb_sr_thr<float, false, 1, kThrS><<<p.grid, kThreads, 0, s>>>(a); break;
-        case 2: k_eb_sr_thr<float, false, 2, kThrS><<<p.grid, kThreads, 0, s>>>(a); break;
-        case 4: k_eb_sr_thr<float, false, 4, kThrS4><<<p.grid, kThreads, 0, s>>>(a); break;
+        case 1: k_eb_sr_thr<float, false, 1, kThrS, NT><<<p.grid, NT, 0, s>>>(a); break;
+        case 2: k_eb_sr_thr<float, false, 2, kThrS, NT><<<p.grid, NT, 0, s>>>(a); break;
+        case 4: k_eb_sr_thr<float, false, 4, kThrS4, NT><<<p.grid, NT, 0, s>>>(a); break;
         default: return cudaErrorNotSupported;
     }
     return cudaGetLastError();
+}
+
+static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.thr_threads == 64) return launch_eb_sr_thr_nt<64>(p, a, s);
+    if (p.thr_threads == 128) return launch_eb_sr_thr_nt<128>(p, a, s);
+    return launch_eb_sr_thr_nt<kThreads>(p, a, s);
 }
 
 template <>

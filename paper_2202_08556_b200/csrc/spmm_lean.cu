@@ -4,15 +4,18 @@
 
 namespace daspmm {
 
-#define DASPMM_LEAN_LPR(KERN, V)                                                      \
+#define DASPMM_LEAN_LPR_NT(KERN, V, NT)                                               \
     switch (p.L) {                                                                   \
-        case 2: KERN<V, 2><<<p.grid, kThreads, 0, s>>>(a); break;                    \
-        case 4: KERN<V, 4><<<p.grid, kThreads, 0, s>>>(a); break;                    \
-        case 8: KERN<V, 8><<<p.grid, kThreads, 0, s>>>(a); break;                    \
-        case 16: KERN<V, 16><<<p.grid, kThreads, 0, s>>>(a); break;                  \
-        case 32: KERN<V, 32><<<p.grid, kThreads, 0, s>>>(a); break;                  \
+        case 2: KERN<V, 2, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
+        case 4: KERN<V, 4, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
+        case 8: KERN<V, 8, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
+        case 16: KERN<V, 16, NT><<<p.grid, NT, 0, s>>>(a); break;                    \
+        case 32: KERN<V, 32, NT><<<p.grid, NT, 0, s>>>(a); break;                    \
         default: return cudaErrorNotSupported;                                       \
     }
+#define DASPMM_LEAN_LPR(KERN, V)                                                      \
+    if (p.lean_threads == 128) { DASPMM_LEAN_LPR_NT(KERN, V, 128) }                  \
+    else { DASPMM_LEAN_LPR_NT(KERN, V, kThreads) }
 
 #define DASPMM_LEAN_V(KERN)                                                           \
     switch (p.V) {                                                                   \

@@ -77,9 +77,39 @@ static cudaError_t launch_rb_sr_repl(const Plan& p, const SpmmArgs<float>& a, cu
     return cudaGetLastError();
 }
 
+// Fast f32 row-major RB+SR in smaller CTAs (Plan::rb_threads; tuning).
+#define DASPMM_RB_NT_TABLE(V, NT)                                                        \
+    switch (p.L) {                                                                      \
+        case 1: k_rb_sr<float, false, false, V, 1, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); break; \
+        case 2: k_rb_sr<float, false, false, V, 2, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); break; \
+        case 4: k_rb_sr<float, false, false, V, 4, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); break; \
+        case 8: k_rb_sr<float, false, false, V, 8, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); break; \
+        case 16: k_rb_sr<float, false, false, V, 16, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); break; \
+        case 32:                                                                        \
+            if (p.X == 2) k_rb_sr<float, false, false, V, 32, 2, kRB, NT><<<p.grid, NT, 0, s>>>(a); \
+            else k_rb_sr<float, false, false, V, 32, 1, kRB, NT><<<p.grid, NT, 0, s>>>(a); \
+            break;                                                                      \
+        default: return cudaErrorNotSupported;                                          \
+    }
+
+template <int NT>
+static cudaError_t launch_rb_sr_nt(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    switch (p.V) {
+        case 1: { DASPMM_RB_NT_TABLE(1, NT) } break;
+        case 2: { DASPMM_RB_NT_TABLE(2, NT) } break;
+        case 4: { DASPMM_RB_NT_TABLE(4, NT) } break;
+        default: return cudaErrorNotSupported;
+    }
+    return cudaGetLastError();
+}
+
 template <>
 cudaError_t launch_rb_sr<float>(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
     if (p.repl) return launch_rb_sr_repl(p, a, s);
+    if (p.rb_threads != kThreads && !p.cm && !p.exact && p.win_rows == 0) {
+        if (p.rb_threads == 64) return launch_rb_sr_nt<64>(p, a, s);
+        if (p.rb_threads == 128) return launch_rb_sr_nt<128>(p, a, s);
+    }
     if (p.win_rows > 0 && !p.cm && !p.exact) return launch_rb_sr_win(p, a, s);
     return launch_rb_sr_rows<float>(p, a, s);
 }

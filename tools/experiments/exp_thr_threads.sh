@@ -1,0 +1,4 @@
+for w in "DASPMM_THR_THREADS=256" "DASPMM_THR_THREADS=128" "DASPMM_THR_THREADS=64"; do
+  echo "== $w"
+  env $w timeout 300 python tools/probe.py --only powerlaw_s20_d16,uniform_s20_d16,banded_s20_b8,powerlaw_s17_d16,uniform_s17_d16,powerlaw_s14_d16 --ns 1,2,4 --kernels 4 --no-torch 2>/dev/null
+done
