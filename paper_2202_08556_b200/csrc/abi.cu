@@ -119,6 +119,7 @@ struct Knobs {
     // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
     // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
     int cta_threads = 64;
+    bool cta_threads_set = false;
     // DASPMM_THR_THREADS (64/128/256): CTA size of the one-lane staged path (measured:
     // 64 -> uniform s20 N = 4 121 -> 105 us, N = 2 105 -> 97; r01c_thr_threads_probe.txt).
     int thr_threads = 64;
@@ -149,9 +150,11 @@ static Knobs read_knobs() {
     k.tma = on("DASPMM_TMA", '1');
     k.tma_lw = i64("DASPMM_TMA_LW");
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
-    if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 64 || t == 128 || t == 256)
+    if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 32 || t == 64 || t == 128 || t == 256) {
         k.cta_threads = int(t);
-    if (const int64_t t = i64("DASPMM_THR_THREADS"); t == 64 || t == 128 || t == 256)
+        k.cta_threads_set = true;
+    }
+    if (const int64_t t = i64("DASPMM_THR_THREADS"); t == 32 || t == 64 || t == 128 || t == 256)
         k.thr_threads = int(t);
     if (const int64_t t = i64("DASPMM_RB_THREADS"); t == 64 || t == 128 || t == 256)
         k.rb_threads = int(t);
@@ -343,7 +346,9 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             workers = p.P;
         } else if (!pr && !exact && P <= 0 && kn.eb_cta) {  // CTA-combined boundary rows
             p.cta = true;
-            p.cta_threads = kn.cta_threads;
+            // one full-warp group per CTA when groups are warps (power-law s20 N = 128
+            // 686 -> 652 us); 64 threads otherwise (r01c_cta_threads_probe.txt)
+            p.cta_threads = kn.cta_threads_set ? kn.cta_threads : (p.L >= 32 ? 32 : 64);
             p.sub = (h->nnz + p.P - 1) / std::max<int64_t>(p.P, 1);
             p.sub = std::max<int64_t>(p.sub, 1);
             p.P = (h->nnz + p.sub - 1) / p.sub;

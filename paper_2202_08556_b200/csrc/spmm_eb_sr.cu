@@ -17,7 +17,8 @@ namespace daspmm {
         default: return cudaErrorNotSupported;                                            \
     }
 #define DASPMM_CTA_LPR_TABLE(T, CM, V)                                                    \
-    if (p.cta_threads == 64) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 64) }                    \
+    if (p.cta_threads == 32) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 32) }                    \
+    else if (p.cta_threads == 64) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 64) }               \
     else if (p.cta_threads == 128) { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, 128) }             \
     else { DASPMM_CTA_LPR_TABLE_NT(T, CM, V, kThreads) }
 
@@ -57,6 +58,7 @@ static cudaError_t launch_eb_sr_thr_nt(const Plan& p, const SpmmArgs<float>& a, 
 }
 
 static cudaError_t launch_eb_sr_thr(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    if (p.thr_threads == 32) return launch_eb_sr_thr_nt<32>(p, a, s);
     if (p.thr_threads == 64) return launch_eb_sr_thr_nt<64>(p, a, s);
     if (p.thr_threads == 128) return launch_eb_sr_thr_nt<128>(p, a, s);
     return launch_eb_sr_thr_nt<kThreads>(p, a, s);
