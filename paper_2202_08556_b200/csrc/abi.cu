@@ -126,9 +126,10 @@ struct Knobs {
     // DASPMM_RB_THREADS (64/128/256): CTA size of fast RB+RM+SR (measured: 128 -> banded
     // s20 N = 8 90 -> 82 us, uniform s20 N = 8 133 -> 123; r01c_rb_threads_probe.txt).
     int rb_threads = 128;
-    // DASPMM_LEAN_THREADS (128/256): CTA size of the lean kernels (measured: 128 -> c3
-    // 3.78 -> 3.69 ms, power-law s20 N = 8 174 -> 156 us; r01c_lean_threads_probe.txt).
-    int lean_threads = 128;
+    // DASPMM_LEAN_THREADS (64/128/256): CTA size of the lean kernels (measured: 128 vs
+    // 256 -> c3 3.78 -> 3.69 ms, power-law s20 N = 8 174 -> 156 us; 64 another ~1%;
+    // r01c_lean_threads_probe.txt).
+    int lean_threads = 64;
 };
 
 static Knobs read_knobs() {
@@ -158,7 +159,7 @@ static Knobs read_knobs() {
         k.thr_threads = int(t);
     if (const int64_t t = i64("DASPMM_RB_THREADS"); t == 64 || t == 128 || t == 256)
         k.rb_threads = int(t);
-    if (const int64_t t = i64("DASPMM_LEAN_THREADS"); t == 128 || t == 256)
+    if (const int64_t t = i64("DASPMM_LEAN_THREADS"); t == 64 || t == 128 || t == 256)
         k.lean_threads = int(t);
     return k;
 }

@@ -14,7 +14,8 @@ namespace daspmm {
         default: return cudaErrorNotSupported;                                       \
     }
 #define DASPMM_LEAN_LPR(KERN, V)                                                      \
-    if (p.lean_threads == 128) { DASPMM_LEAN_LPR_NT(KERN, V, 128) }                  \
+    if (p.lean_threads == 64) { DASPMM_LEAN_LPR_NT(KERN, V, 64) }                    \
+    else if (p.lean_threads == 128) { DASPMM_LEAN_LPR_NT(KERN, V, 128) }             \
     else { DASPMM_LEAN_LPR_NT(KERN, V, kThreads) }
 
 #define DASPMM_LEAN_V(KERN)                                                           \
