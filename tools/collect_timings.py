@@ -32,8 +32,9 @@ def corpus(quick: bool):
             specs.append(("uniform", s, deg, None))
             for a in (0.45, 0.57, 0.7):
                 specs.append(("rmat", s, deg, a))
-        if not quick and s in (12, 16, 20):
+        if not quick and s in (12, 14, 16, 17, 18, 20):
             specs.append(("banded", s, 4, None))
+            specs.append(("banded", s, 8, None))
             specs.append(("banded", s, 32, None))
         if not quick and s in (11, 12, 13, 14):  # small, denser matrices (c1-like: 4096^2, 1%)
             for deg in (40, 128):
