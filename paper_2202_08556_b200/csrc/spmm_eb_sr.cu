@@ -83,15 +83,19 @@ cudaError_t launch_eb_prep_uniform(const int* rows, int64_t nnz, int64_t sub, in
     const bool v4 = sizeof(T) == 4 && N % 4 == 0 && ldc % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(C) & 15) == 0;
     const int vz = v4 ? 4 : 1;
-    const int64_t work = (n_bound + n_empty) * ((N + vz - 1) / vz);
+    const int64_t nvec = (N + vz - 1) / vz;
+    const int64_t work = (n_bound + n_empty) * nvec;
     if (work == 0) return cudaSuccess;
     const dim3 grid(unsigned((work + kThreads - 1) / kThreads));
+    int shift = -1;
+    if ((nvec & (nvec - 1)) == 0 && int64_t(grid.x) * kThreads < (int64_t(1) << 32))
+        for (shift = 0; (int64_t(1) << shift) < nvec; ++shift) {}
     if (v4)
         k_eb_prep_uniform<T, (sizeof(T) == 4 ? 4 : 1)><<<grid, kThreads, 0, s>>>(
-            rows, nnz, stride, n_bound, C, ldc, N, empty_rows, n_empty);
+            rows, nnz, stride, n_bound, C, ldc, N, empty_rows, n_empty, shift);
     else
         k_eb_prep_uniform<T, 1><<<grid, kThreads, 0, s>>>(rows, nnz, stride, n_bound, C, ldc, N,
-                                                          empty_rows, n_empty);
+                                                          empty_rows, n_empty, shift);
     return cudaGetLastError();
 }
 template cudaError_t launch_eb_prep_uniform<float>(const int*, int64_t, int64_t, int64_t, int,
