@@ -10,19 +10,21 @@
 //     indices and one of 4 values, every lane of the group at the same address
 //     (one L1 wavefront, broadcast) — instead of per-lane loads plus two shuffles
 //     per nonzero;
-//   * a group walks a contiguous nonzero range in 8-element blocks; the COO row ids
-//     arrive as quads too, and a block that stays inside the current row (the common
-//     case) runs branch-free — one compare per block instead of row tracking per
-//     nonzero; masked slots (range edges) issue no load and no FFMA;
+//   * walks: one row segment at a time (segment walk; next row from the COO id at the
+//     segment end), or a contiguous nonzero range in 8-element blocks with the COO row
+//     ids loaded as quads too (range walk): a block that stays inside the current row
+//     runs branch-free; masked slots (range edges) issue no load and no FFMA;
 //   * two quads per iteration: 8 independent B-row gathers in flight per lane before
 //     the 32 FFMAs that consume them.
 //
-//   RB (K0): group owns rows [g*rpg, (g+1)*rpg); every row is stored once (empty rows
-//            are zeroed by the prologue).
-//   EB (K4): group owns the nnz chunk [w*chunk, (w+1)*chunk) (partition_elements with
-//            equal chunks); a row wholly inside the chunk is stored, a row cut by the
-//            chunk's ends takes a vector atomic add (pre-zeroed by k_eb_prep_uniform),
-//            empty rows are pre-zeroed.
+//   RB (K0, opt-in DASPMM_LEAN_RB=1): group owns rows [g*rpg, (g+1)*rpg), one segment
+//            per row, every row stored (empty rows store zeros).
+//   EB (K4, N <= 16 or long rows): group owns the nnz chunk [w*chunk, (w+1)*chunk); a
+//            row wholly inside the chunk is stored, a row cut by the chunk's ends takes
+//            a vector atomic add (pre-zeroed by k_eb_prep_uniform), empty rows are
+//            pre-zeroed.
+// Where each wins is measured in DESIGN.md §3.1; CTA size is a template parameter
+// (64 threads by default, Plan::lean_threads).
 //
 // Requires ci/va/rows 16-byte aligned (quad loads) and ldb * 4 < 2^31 (plan_spmm checks);
 // the last partial quad of the arrays is read with scalar loads so nothing past nnz is
@@ -33,10 +35,10 @@
 
 namespace daspmm {
 
-// Resident CTAs per SM the lean kernels are compiled for (register cap 65536 / (256 x
-// minB)). Measured on B200: the RB walk gains from 4 (64 registers, 32 warps: uniform
-// s20 N = 128 1294 -> 1245 us), the EB walks lose at 4 (power-law N = 16 range walk
-// 217 -> 303 us) and keep 3 (80 registers).
+// Resident 256-thread CTAs per SM the lean kernels are compiled for (register cap 65536
+// / (256 x minB); scaled for smaller CTAs). Measured on B200: the RB walk gains from 4
+// (64 registers, 32 warps: uniform s20 N = 128 1294 -> 1245 us), the EB walks lose at 4
+// (power-law N = 16 range walk 217 -> 303 us) and keep 3 (80 registers).
 constexpr int kLeanMinBlocksRB = 4;
 constexpr int kLeanMinBlocksEB = 3;
 
