@@ -276,13 +276,13 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     // quad-aligned A arrays. One column slot per lane; wider N takes more y-tiles.
     p.lean = !base_only && !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 &&
              kn.lean &&
-             p.L >= kn.lean_min_lanes && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
+             (p.L >= kn.lean_min_lanes || (!eb && p.L == 1)) && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
              (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
                                            reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
     // Where the lean walks win (measured on B200 against the shuffle-broadcast walks with
     // their one-IMAD gather addressing, profiles/r01_notes.md step 17):
-    //   RB: nowhere by more than noise (uniform s20 N = 8 130 vs 134 us; N = 128 1246 vs
-    //       1229), so k_rb_sr keeps RB unless DASPMM_LEAN_RB=1;
+    //   RB: one-lane groups only (below); elsewhere they tie within noise (uniform s20
+    //       N = 8 130 vs 134 us; N = 128 1246 vs 1229);
     //   EB: N <= 16 (power-law s20 N = 8 160 vs 279, N = 16 199 vs 240) and long rows at
     //       any N (c3 3.77 vs 3.99 ms); from N = 32 on short rows the CTA-combined walk
     //       with 256-pair chunks wins (power-law s20 N = 32 326 vs 271, N = 128 957 vs
@@ -290,7 +290,10 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     const double avg_nonempty =
         h->M > h->n_empty ? double(h->nnz) / double(h->M - h->n_empty) : 0.0;
     const bool lean_ok = p.lean;  // eligibility (also of the TMA-gather variant)
-    if (p.lean && !eb) p.lean = kn.lean_rb;
+    // RB: one-lane groups (N <= 4) take the lean walk — quad loads of each row's pairs
+    // instead of 8 scalar loads per lane (uniform s20 N = 2 107 -> 96 us, banded 51 -> 47);
+    // wider groups tie with k_rb_sr and stay on it unless DASPMM_LEAN_RB=1.
+    if (p.lean && !eb) p.lean = kn.lean_rb || p.L == 1;
     if (p.lean && eb && N > 16 && avg_nonempty < 48.0) p.lean = false;
     if (p.lean) {
         p.X = 1;

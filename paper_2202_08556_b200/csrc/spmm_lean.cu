@@ -6,6 +6,7 @@ namespace daspmm {
 
 #define DASPMM_LEAN_LPR_NT(KERN, V, NT)                                               \
     switch (p.L) {                                                                   \
+        case 1: KERN<V, 1, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
         case 2: KERN<V, 2, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
         case 4: KERN<V, 4, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
         case 8: KERN<V, 8, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
