@@ -257,7 +257,15 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             p.V /= 2;
         }
     }
-    const int64_t ncols = std::min<int64_t>(N, max_tile_cols(kn));
+    int64_t tile_max = max_tile_cols(kn);
+    // RB+RM+SR with B far beyond L2 (>= 256 MB): two 64-column y-tiles run one after the
+    // other, halving the B working set each pass must find in L2 (uniform s20 N = 128,
+    // B 512 MB: 1204 -> 1137 us). Below that the second pass over A costs more than the
+    // hits gain (c3, B 119 MB: 5.35 -> 7.20 ms; profiles/r01c_tile64_probe.txt).
+    if (kn.tile_cols <= 0 && !eb && !pr && !p.cm && !exact && N > 64 && N <= 128 &&
+        h->K * N * elem_size(h->dtype) >= (int64_t(256) << 20))
+        tile_max = 64;
+    const int64_t ncols = std::min<int64_t>(N, tile_max);
     const int64_t nv = (ncols + p.V - 1) / p.V;  // column slots per tile
     int64_t tile_cols;
     int lanes;
@@ -276,7 +284,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
     // quad-aligned A arrays. One column slot per lane; wider N takes more y-tiles.
     p.lean = !base_only && !pr && !exact && !p.cm && h->dtype == DASPMM_F32 && P <= 0 &&
              kn.lean &&
-             (p.L >= kn.lean_min_lanes || (!eb && p.L == 1)) && ldb < (int64_t(1) << 29) && h->coo_rows != nullptr &&
+             (p.L >= kn.lean_min_lanes || (!eb && p.L == 1)) && ldb < (int64_t(1) << 29) &&
+             h->coo_rows != nullptr &&
              (((reinterpret_cast<uintptr_t>(h->ci) | reinterpret_cast<uintptr_t>(h->coo_rows) |
                                            reinterpret_cast<uintptr_t>(h->va)) & 15) == 0);
     // Where the lean walks win (measured on B200 against the shuffle-broadcast walks with
