@@ -201,7 +201,7 @@ int daspmm_spmm_rows_to(const daspmm_csr* csr, const void* d_B, int64_t ldb, int
 int daspmm_reload_env(void);
 
 /* Which launch variant daspmm_spmm would run for these operands (no launch):
- *   variant 0 = the design point's base kernel, 1 = RB+SR with the B window staged in
+ *   variant 0 = the design point's base kernel (*param = column tiles, grid.y), 1 = RB+SR with the B window staged in
  *   shared memory (*param = rows per CTA panel), 2 = EB+SR with CTA-combined boundary
  *   rows, 3 = EB+SR one-lane staged sub-chunks (*param = pairs per thread), 4 = lean
  *   SR kernel (*param = rows per group for RB, pairs per chunk for EB), 5 = EB+SR with

@@ -258,12 +258,15 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         }
     }
     int64_t tile_max = max_tile_cols(kn);
-    // RB+RM+SR with B far beyond L2 (>= 256 MB): two 64-column y-tiles run one after the
-    // other, halving the B working set each pass must find in L2 (uniform s20 N = 128,
-    // B 512 MB: 1204 -> 1137 us). Below that the second pass over A costs more than the
-    // hits gain (c3, B 119 MB: 5.35 -> 7.20 ms; profiles/r01c_tile64_probe.txt).
+    // RB+RM+SR with B far beyond L2 (>= 256 MB) and scattered columns (32-row panels span
+    // over a quarter of K): two 64-column y-tiles run one after the other, halving the B
+    // working set each pass must find in L2 (uniform s20 N = 128, B 512 MB: 1204 -> 1137
+    // us). Below that size, or with row-local columns (banded s20: 454 -> 515 us), the
+    // second pass over A costs more than the hits gain (c3, B 119 MB: 5.35 -> 7.20 ms;
+    // profiles/r01c_tile64_probe.txt).
     if (kn.tile_cols <= 0 && !eb && !pr && !p.cm && !exact && N > 64 && N <= 128 &&
-        h->K * N * elem_size(h->dtype) >= (int64_t(256) << 20))
+        h->K * N * elem_size(h->dtype) >= (int64_t(256) << 20) && h->spans != nullptr &&
+        h->span_avg[0] * 4.0 >= double(h->K))
         tile_max = 64;
     const int64_t ncols = std::min<int64_t>(N, tile_max);
     const int64_t nv = (ncols + p.V - 1) / p.V;  // column slots per tile
@@ -943,7 +946,7 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
     const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
     *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
     *param = p.win_rows > 0 ? p.win_rows : (p.thr || p.tma || (p.lean && kernel >= 4)) ? p.sub
-             : p.lean ? p.rpg : 0;
+             : p.lean ? p.rpg : int64_t(p.grid.y);
     return DASPMM_OK;
 }
 

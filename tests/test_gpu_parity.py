@@ -525,6 +525,60 @@ def test_lean_sr_kernels(sk, kernel, skew):
 
 
 @pytest.mark.parametrize("skew", [0.0, 1.3])
+def test_rb_lean_one_lane_default(sk, skew):
+    """RB+RM+SR with one-lane groups (N <= 4) runs the lean quad-load walk by default:
+    odd nnz, empty and long rows, padded ldb; within the gamma bound, C fully written."""
+    import torch
+
+    a = H.random_csr(4099, 3001, 70001, seed=23, dtype=np.float32, skew=skew)
+    d = sk.DeviceCsr.from_host(a)
+    for n in (1, 2, 3, 4):
+        x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
+        y64 = O.spmm_reference(H.to_oracle(a), x.astype(np.float64))
+        bound = H.gamma_bound(a, x, np.float32)
+        for padded in (False, True):
+            B = torch.zeros(a.num_cols, n + 5 * padded, device="cuda")[:, :n]
+            B.copy_(torch.from_numpy(x))
+            C = torch.full((a.num_rows, n), float("nan"), device="cuda")
+            if n in (2, 4) and not padded:
+                assert sk.plan_info(0, d, B, C)[0] == "lean"
+            sk.spmm_device(0, d, B, C)
+            torch.cuda.synchronize()
+            err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= bound).all(), f"n{n} padded={padded}: {np.nanmax(err)}"
+
+
+def test_rb_column_tiles_for_wide_b(sk):
+    """B beyond 256 MB (K = 2^19, N = 128 fp32) makes RB+RM+SR run two 64-column tiles;
+    the result is checked on the touched B rows against an fp64 restatement."""
+    import torch
+
+    K, M, nnz, n = 1 << 19, 3001, 60001, 128
+    rng = np.random.default_rng(5)
+    a = H.random_csr(M, K, nnz, seed=29, dtype=np.float32)
+    d = sk.DeviceCsr.from_host(a)
+    B = torch.empty(K, n, device="cuda").uniform_(-1, 1, generator=torch.Generator(
+        device="cuda").manual_seed(int(rng.integers(1 << 30))))
+    C = torch.full((M, n), float("nan"), device="cuda")
+    assert sk.plan_info(0, d, B, C) == ("base", 2)
+    sk.spmm_device(0, d, B, C)
+    torch.cuda.synchronize()
+    ci = torch.from_numpy(a.col_indices.astype(np.int64)).cuda()
+    xs = B[ci].double().cpu().numpy()  # the gathered rows, in nnz order
+    rows = np.repeat(np.arange(M), np.diff(a.row_offsets))
+    prod = a.values.astype(np.float64)[:, None] * xs
+    y64 = np.zeros((M, n))
+    np.add.at(y64, rows, prod)
+    mag = np.zeros((M, n))
+    np.add.at(mag, rows, np.abs(prod))
+    lens = np.diff(a.row_offsets).astype(np.float64)
+    u = 2.0 ** -24
+    bound = 2 * ((lens + 1) * u / (1 - (lens + 1) * u))[:, None] * mag + 1e-30
+    err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
+    assert (err <= bound).all(), np.nanmax(err)
+
+
+@pytest.mark.parametrize("skew", [0.0, 1.3])
 def test_eb_tma_gather_kernel(sk, skew):
     """EB+RM+SR with TMA gather4 row fetches (DASPMM_TMA=1): box widths 32/64/128 with
     zero-filled columns past N, several y-tiles, padded ldb, odd nnz (array-tail stage),
