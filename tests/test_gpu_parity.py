@@ -526,11 +526,12 @@ def test_lean_sr_kernels(sk, kernel, skew):
 
 @pytest.mark.parametrize("skew", [0.0, 1.3])
 def test_rb_lean_one_lane_default(sk, skew):
-    """RB+RM+SR with one-lane groups (N <= 4) runs the lean quad-load walk by default:
-    odd nnz, empty and long rows, padded ldb; within the gamma bound, C fully written."""
+    """RB+RM+SR with one-lane groups (N <= 4) runs the lean quad-load walk by default
+    (M large enough that the planner keeps V = N, i.e. one lane per row): odd nnz, empty
+    and long rows, padded ldb; within the gamma bound, C fully written."""
     import torch
 
-    a = H.random_csr(4099, 3001, 70001, seed=23, dtype=np.float32, skew=skew)
+    a = H.random_csr(80003, 3001, 700001, seed=23, dtype=np.float32, skew=skew)
     d = sk.DeviceCsr.from_host(a)
     for n in (1, 2, 3, 4):
         x = np.random.default_rng(n).uniform(-1, 1, (a.num_cols, n)).astype(np.float32)
