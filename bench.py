@@ -8,7 +8,7 @@ selector plus the selected sm_100a kernel, dispatched on the device through a CU
 graph SWITCH node — once for every (matrix, N) pair of the suite.
 
   value     suite GFLOP/s = sum(2*nnz*N) / sum(device time), inputs resident in HBM,
-            L2 flushed (256 MiB write) before every call, CUDA events per call.
+            L2 flushed (256 MiB read sweep) before every call, CUDA events per call.
   e2e       same metric through the public API with host operands: pinned-host B ->
             device, DA-SpMM, C -> pinned host, all inside the timed region.
   roofline  HBM roofline of the step: algorithmic bytes (SURVEY §8d:
@@ -106,6 +106,13 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _flush(buf):
+    """Evicts L2 between timed calls with a READ sweep of a buffer twice the L2 size:
+    the lines it leaves are clean, so the next call pays no write-back for them (a
+    zero-fill would leave up to 126 MB of dirty lines for the timed call to drain)."""
+    buf.sum()
+
+
 def _max_over_ranks(v: float, dev) -> float:
     """Max of a per-rank scalar over all ranks (device tensor for NCCL, host for gloo)."""
     import torch
@@ -197,7 +204,7 @@ def run_ours(args):
     sk.lib()  # fail loudly if the CUDA library is missing
     model = sk.load_selector(open(args.model).read())
     mats = build_suite(args.small, rank, world, args.workload)
-    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flush = torch.ones(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     ns_override = [int(n) for n in args.ns.split(",")] if args.ns else None
     ns = sorted({n for m in mats for n in (ns_override or m["ns"])})
 
@@ -218,7 +225,7 @@ def run_ours(args):
 
     def step(times=None):
         for i, c in enumerate(calls):
-            flush.zero_()
+            _flush(flush)
             if times is None:
                 one(c)
             else:
@@ -278,7 +285,9 @@ def run_ours(args):
         e2e = None  # operands too large to stage in pinned host memory (c5: 68 GB)
     else:
         e2e = _e2e(calls, one, stream, args, world, total_flops)
-    parity = _spot_check(calls[dom]) if rank == 0 else None
+    parity = _parity_map(calls) if rank == 0 else None
+    warm = _warm(calls, one, stream, world, dev, total_flops)
+    overhead = _da_overhead(calls, model, stream, flush) if rank == 0 else None
     assembly = None
     if world > 1:
         try:
@@ -289,7 +298,108 @@ def run_ours(args):
         _write_roofline_table(args.roofline_table, calls, per_call_ms, chosen, peak)
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-                   flush, assembly)
+                   flush, assembly, warm, overhead)
+
+
+def _warm(calls, one, stream, world, dev, total_flops, reps=3):
+    """The same calls with a warm L2 (no flush; each call run `reps` times back to back,
+    the mean of the last reps-1 taken): the figure beside the cold, flushed one."""
+    import torch
+
+    per = []
+    for c in calls:
+        one(c)
+        evs = []
+        for _ in range(reps):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            one(c)
+            e.record(stream)
+            evs.append((s, e))
+        torch.cuda.synchronize()
+        per.append(sum(s.elapsed_time(e) for s, e in evs[1:]) / (reps - 1))
+    ms = sum(per)
+    if world > 1:
+        ms = _max_over_ranks(ms, dev)
+    dom = max(range(len(calls)), key=lambda i: per[i])
+    return {"value": round(total_flops / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "ms_per_step": round(ms, 4),
+            "dominant": {"call": f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}',
+                         "ms": round(per[dom], 4)},
+            "protocol": f"no L2 flush; each call {reps}x back to back, mean of the last {reps - 1}"}
+
+
+def _da_overhead(calls, model, stream, flush, reps=3):
+    """Uncached DA-SpMM: per call, the device selector (ensemble walk) + SWITCH dispatch +
+    the chosen kernel (DASPMM_RESELECT), against the steady-state call that launches the
+    published choice directly, and against a plain daspmm_spmm of that kernel. L2 flushed
+    before every run; CUDA events on the launching stream."""
+    import torch
+
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    def timed(fn):
+        tot = 0.0
+        for _ in range(reps):
+            _flush(flush)
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            fn()
+            e.record(stream)
+            torch.cuda.synchronize()
+            tot += s.elapsed_time(e)
+        return tot / reps
+
+    resel, direct, plain = 0.0, 0.0, 0.0
+    for c in calls:
+        kid = int(c["kout"].item())
+        sk.spmm_selected(c["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream,
+                         reselect=True)  # builds the reselect graph outside the timing
+        resel += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"],
+                                                kernel_out=c["kout"], stream=stream,
+                                                reselect=True))
+        direct += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"],
+                                                 kernel_out=c["kout"], stream=stream))
+        Bk = c["B"].t().contiguous() if (kid >> 1) & 1 else c["B"]
+        plain += timed(lambda: sk.spmm_device(kid, c["d"], Bk, c["C"], stream=stream))
+    n = len(calls)
+    return {"reselect_ms_per_step": round(resel, 4), "direct_ms_per_step": round(direct, 4),
+            "plain_kernel_ms_per_step": round(plain, 4),
+            "selector_dispatch_us_per_call": round((resel - direct) / n * 1e3, 2),
+            "cached_dispatch_us_per_call": round((direct - plain) / n * 1e3, 2),
+            "note": "reselect = device selector walk + graph SWITCH + kernel every call "
+                    "(the reference's per-call predict_kernel flow, spmmkit_cli.cpp:239-270); "
+                    "direct = published choice launched directly; plain = daspmm_spmm of the "
+                    "same kernel (CM kernels on a pre-transposed B)"}
+
+
+def _parity_map(calls):
+    """Every timed call checked against the fp64 oracle on sampled rows (oracle/sampled.py:
+    random rows + rows straddling EB chunk / CTA boundaries), outside the timed region."""
+    import numpy as np
+
+    from oracle import sampled as S
+
+    out, fails, worst = {}, [], 0.0
+    for c in calls:
+        m = c["m"]
+        r0, r1 = c["rows"]
+        rp_h = m["rp"][r0:r1 + 1].cpu().numpy().astype(np.int64)
+        rp_h = rp_h - rp_h[0]
+        rows = S.sample_rows(rp_h, n_random=128, n_boundary=8, seed=c["n"])
+        res = S.check(m["rp"], m["ci"], m["va"], m["K"], c["B"], c["C"], rows + r0, row0=r0)
+        key = f'{m["name"]}/N{c["n"]}'
+        out[key] = round(res["max_ratio"], 4)
+        worst = max(worst, res["max_ratio"])
+        if not res["ok"]:
+            fails.append(key)
+    return {"calls_checked": len(calls), "calls_passed": len(calls) - len(fails),
+            "failed": fails, "worst_err_over_bound": round(worst, 4),
+            "check": "fp64 oracle on sampled rows (random + EB/CTA boundary rows); "
+                     "|y - y64| <= 2 gamma(len+1) sum|a x|",
+            "err_over_bound_per_call": out}
 
 
 def _assembly(calls, mats, world, dev):
@@ -406,7 +516,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
 
 def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
             per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-            flush, assembly=None):
+            flush, assembly=None, warm=None, overhead=None):
     import torch.distributed as dist
 
     from paper_2202_08556_b200 import spmmkit as sk
@@ -425,7 +535,7 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                                + " N=" + ",".join(map(str, ns)),
                    "matrices": [m["name"] for m in mats], "ns": ns,
                    "calls_per_step": len(calls), "selector": os.path.basename(args.model),
-                   "l2": "flushed (256 MiB write) before every timed call",
+                   "l2": "flushed before every timed call (read sweep of 256 MiB, clean lines)",
                    "parallelism": (f"{world} GPUs: calls sharded by multi.schedule_units (large calls "
                                    "as nnz-balanced row panels, B replicated; the rest whole, LPT)")
                                   if world > 1 else "1 GPU"},
@@ -450,6 +560,8 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
         "per_call_ms": {f'{c["m"]["name"]}/N{c["n"]}': round(t, 5)
                         for c, t in zip(calls, per_call_ms)},
         "parity": parity,
+        "warm_l2": warm,
+        "da_spmm_overhead": overhead,
     }
     if assembly is not None:
         result["assembly"] = assembly
@@ -518,39 +630,16 @@ def _ceilings(c, traffic, peak):
     return out
 
 
-def _spot_check(c):
-    """fp64 oracle on a sample of rows of the dominant call (gamma bound)."""
-    import numpy as np
-
-    from oracle import oracle as O
-
-    m = c["m"]
-    r0, r1 = c["rows"]
-    rp = m["rp"].cpu().numpy().astype(np.int64)[r0:r1 + 1]
-    rows = np.unique(np.linspace(0, r1 - r0 - 1, num=min(512, r1 - r0)).astype(np.int64))
-    sub_rp = [0]
-    sub_ci, sub_va = [], []
-    for r in rows:  # slice on the device, copy only the sampled rows
-        s, e = int(rp[r]), int(rp[r + 1])
-        sub_ci.append(m["ci"][s:e].cpu().numpy().astype(np.int64))
-        sub_va.append(m["va"][s:e].cpu().numpy().astype(np.float64))
-        sub_rp.append(sub_rp[-1] + (e - s))
-    a = O.Csr(len(rows), m["K"], np.array(sub_rp), np.concatenate(sub_ci), np.concatenate(sub_va))
-    x = c["B"].cpu().numpy().astype(np.float64)
-    y64 = O.spmm_reference(a, x)
-    absa = O.Csr(a.num_rows, a.num_cols, a.row_offsets, a.col_indices, np.abs(a.values))
-    mag = O.spmm_reference(absa, np.abs(x))
-    lens = np.diff(a.row_offsets).astype(np.float64)
-    u = 2.0 ** -24
-    bound = 2 * ((lens + 1) * u / (1 - (lens + 1) * u))[:, None] * mag + 1e-30
-    y = c["C"].cpu().numpy()[rows].astype(np.float64)
-    ok = bool((np.abs(y - y64) <= bound).all())
-    return {"call": f'{m["name"]}/N{c["n"]}', "rows_checked": int(len(rows)), "within_gamma": ok,
-            "max_abs_err": float(np.abs(y - y64).max()) if y.size else 0.0}
+CUSPARSE_ALGS = ("DEFAULT", "CSR_ALG1", "CSR_ALG2", "CSR_ALG3", "COO_ALG1", "COO_ALG2",
+                 "COO_ALG3", "COO_ALG4")
 
 
-def _cusparse_compare(calls, flush, our_ms, ns):
-    """Best of cuSPARSE CSR algorithms per call, same operands, same L2 flush."""
+def _cusparse_compare(calls, flush, our_ms, ns, reps=5):
+    """Best cuSPARSE SpMM per call over every CSR and COO algorithm with B and C
+    row-major and column-major (PAPER.md:420's baseline set minus the blocked formats),
+    on the same matrix, the same L2 flush before every timed run and the same statistic
+    as our calls (mean of `reps` runs). Column-major operands are prepared outside the
+    timed region; CSR_ALG3's preprocessing too (cmp_create)."""
     import torch
 
     from paper_2202_08556_b200 import build
@@ -559,40 +648,57 @@ def _cusparse_compare(calls, flush, our_ms, ns):
     if not os.path.exists(path):
         return None
     L = C.CDLL(path)
-    L.cmp_create.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 4 + [C.c_int64] * 2 + \
-        [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.cmp_create.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 5 + [C.c_int64] * 2 + \
+        [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
     L.cmp_run.argtypes = [C.c_void_p]
     L.cmp_destroy.argtypes = [C.c_void_p]
     stream = torch.cuda.current_stream()
-    best = []
+    best, winner = [], []
     for c in calls:
         d = c["d"]
         rp, ci, va = d.device_arrays()
+        rp_t = c["m"]["rp"]
+        r0, r1 = c["rows"]
+        lens = (rp_t[r0 + 1:r1 + 1] - rp_t[r0:r1]).to(torch.int64)
+        coo = torch.repeat_interleave(torch.arange(d.num_rows, device=lens.device,
+                                                   dtype=torch.int32), lens)
+        n = c["n"]
         out = torch.empty_like(c["C"])
+        Bcm = c["B"].t().contiguous()                      # N x K buffer = column-major K x N
+        out_cm = torch.empty(n, d.num_rows, device=out.device)  # column-major M x N
         ts = {}
-        for alg in (0, 1, 2, 3):
-            h = C.c_void_p()
-            if L.cmp_create(d.num_rows, d.num_cols, d.nnz(), rp, ci, va, c["B"].data_ptr(), c["n"],
-                            c["n"], out.data_ptr(), c["n"], alg, stream.cuda_stream,
-                            C.byref(h)) != 0:
-                continue
-            if L.cmp_run(h) != 0:
-                L.cmp_destroy(h)
-                continue
-            L.cmp_run(h)
-            samples = []
-            for _ in range(3):
-                flush.zero_()
-                s = torch.cuda.Event(enable_timing=True)
-                e = torch.cuda.Event(enable_timing=True)
-                s.record(stream)
-                L.cmp_run(h)
-                e.record(stream)
+        for order in (0, 1):
+            for alg in range(len(CUSPARSE_ALGS)):
+                h = C.c_void_p()
+                Bp, ldb = (c["B"].data_ptr(), n) if order == 0 else (Bcm.data_ptr(), d.num_cols)
+                Cp, ldc = (out.data_ptr(), n) if order == 0 else (out_cm.data_ptr(), d.num_rows)
+                if L.cmp_create(d.num_rows, d.num_cols, d.nnz(), rp, ci, coo.data_ptr(), va, Bp,
+                                n, ldb, Cp, ldc, order, alg, stream.cuda_stream, C.byref(h)) != 0:
+                    continue
+                if L.cmp_run(h) != 0:
+                    L.cmp_destroy(h)
+                    continue
                 torch.cuda.synchronize()
-                samples.append(s.elapsed_time(e))
-            ts[alg] = sorted(samples)[1]
-            L.cmp_destroy(h)
-        best.append(min(ts.values()) if ts else float("nan"))
+                tot = 0.0
+                for _ in range(reps):
+                    _flush(flush)
+                    s = torch.cuda.Event(enable_timing=True)
+                    e = torch.cuda.Event(enable_timing=True)
+                    s.record(stream)
+                    L.cmp_run(h)
+                    e.record(stream)
+                    torch.cuda.synchronize()
+                    tot += s.elapsed_time(e)
+                ts[(order, alg)] = tot / reps
+                L.cmp_destroy(h)
+        if ts:
+            k = min(ts, key=ts.get)
+            best.append(ts[k])
+            winner.append(("row" if k[0] == 0 else "col") + ":" + CUSPARSE_ALGS[k[1]])
+        else:
+            best.append(float("nan"))
+            winner.append(None)
+        del Bcm, out_cm, out, coo
     tot_flops = sum(c["flops"] for c in calls)
     cus_ms = sum(best)
     speedups = [b / o for b, o in zip(best, our_ms) if o > 0]
@@ -600,10 +706,18 @@ def _cusparse_compare(calls, flush, our_ms, ns):
     by_n = {}
     for c, b, o in zip(calls, best, our_ms):
         by_n.setdefault(c["n"], []).append(b / o)
+    wins = {}
+    for w in winner:
+        wins[w] = wins.get(w, 0) + 1
     return {"value": round(tot_flops / (cus_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
-            "best_alg_per_call": True, "ms_per_step": round(cus_ms, 4),
+            "best_alg_per_call": True,
+            "algorithms": [f"{o}:{a}" for o in ("row", "col") for a in CUSPARSE_ALGS],
+            "statistic": f"mean of {reps} runs, L2 flushed before each (same as ours)",
+            "ms_per_step": round(cus_ms, 4),
             "per_call_ms": {f'{c["m"]["name"]}/N{c["n"]}': round(b, 5)
                             for c, b in zip(calls, best)},
+            "winner_per_call": {f'{c["m"]["name"]}/N{c["n"]}': w for c, w in zip(calls, winner)},
+            "winner_counts": wins,
             "speedup_geomean": round(geo, 4) if geo else None,
             "speedup_geomean_by_N": {str(n): round(statistics.geometric_mean(v), 4)
                                      for n, v in sorted(by_n.items())}}

@@ -57,7 +57,11 @@ enum {
      * reference's spmm() bit for bit (RB kernels always; EB kernels on rows owned by
      * one chunk, with P honoured as the chunk count). Default: fused multiply-add,
      * library-chosen EB chunking, tolerance parity. */
-    DASPMM_EXACT = 1u
+    DASPMM_EXACT = 1u,
+    /* daspmm_spmm_selected only: run the device selector (ensemble walk) and the SWITCH
+     * dispatch on this call even when the choice for (matrix, model, N, hw) is already
+     * known — measures the uncached DA-SpMM overhead. */
+    DASPMM_RESELECT = 2u
 };
 
 /* Human-readable message for the last failing call on this thread. */
@@ -170,14 +174,22 @@ int daspmm_select(const daspmm_csr* csr, const daspmm_model* model, int64_t n_co
  * conditional node; the selector kernel sets the branch). B may be in either
  * layout; a body whose kernel needs the other layout converts B on the device
  * first, as spmm_auto_layout does. W/Cb from make_config(kernel, N) defaults
- * (worker.hpp:47-55) unless W > 0. Optional d_kernel receives the choice. The
- * instantiated graph is cached per (operands, N, stream); repeated calls are one
- * graph launch. */
+ * (worker.hpp:47-55) unless W > 0. Optional d_kernel receives the choice.
+ * Caching: the choice depends only on (matrix, model, N, hw). Until the device has
+ * published it, calls run the graph (at most 4 instantiated graphs per handle, LRU);
+ * afterwards every call with that key — any B, C or stream — launches the chosen kernel
+ * directly (DASPMM_RESELECT forces the graph path). Memory stays bounded however many
+ * distinct operand buffers are used. Models with more than 8 classes are rejected with
+ * DASPMM_ERR_OUT_OF_RANGE (KernelId::from_index, kernel_id.hpp:30). */
 int daspmm_spmm_selected(const daspmm_csr* csr, const daspmm_model* model, int64_t hw,
                          const void* d_B, int b_layout, int64_t ldb, int64_t N, void* d_C,
                          int64_t ldc, int64_t W, unsigned flags, int* d_kernel,
                          daspmm_stream stream);
 
+/* Graph-cache occupancy of a handle: instantiated graphs, retired graphs awaiting
+ * completion, and known (model, N, hw) decisions. Diagnostics for tests. */
+int daspmm_selected_cache_info(const daspmm_csr* csr, int64_t* graphs, int64_t* retired,
+                               int64_t* decided);
 /* ----------------------------------------------------------- test hooks (device) */
 
 /* The device warp primitives on caller data, for bit-exact checks against

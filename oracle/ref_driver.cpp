@@ -202,13 +202,17 @@ int ref_time_spmm_f32(void* hp, int kernel, int64_t P, int64_t W, int64_t C, con
                       double* checksum) {
     auto* h = static_cast<RefCsr*>(hp);
     return guarded([&] {
-        const auto xk = dense_from(x, h->f.num_cols, n, (kernel >> 1) & 1);
-        const KernelId k = KernelId::from_index(kernel);
+        // kernel -1: spmm_reference (spmm.hpp:16-32), serial, row-major X
+        const auto xk = dense_from(x, h->f.num_cols, n, kernel >= 0 && ((kernel >> 1) & 1));
+        const KernelId k = KernelId::from_index(kernel >= 0 ? kernel : 0);
         const WorkerConfig cfg{P, W, C};
         FeatureVector fv;
         fv.n_cols = n;
-        auto rec = time_kernel_fn<float>([&] { return spmm(k, h->f, xk, cfg); }, nullptr,
-                                         "bench", fv, k, reps, warmup);
+        auto rec = kernel >= 0
+                       ? time_kernel_fn<float>([&] { return spmm(k, h->f, xk, cfg); }, nullptr,
+                                               "bench", fv, k, reps, warmup)
+                       : time_kernel_fn<float>([&] { return spmm_reference(h->f, xk); }, nullptr,
+                                               "bench", fv, k, reps, warmup);
         *median_s = rec.median_time;
         *min_s = rec.min_time;
         *checksum = rec.checksum;

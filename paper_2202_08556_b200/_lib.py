@@ -23,6 +23,7 @@ ERR_UNSUPPORTED = 9
 F32, F64 = 0, 1
 ROW_MAJOR, COL_MAJOR = 0, 1
 EXACT = 1
+RESELECT = 2
 
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -61,6 +62,7 @@ SIGNATURES = {
     "daspmm_reload_env": (C.c_int, []),
     "daspmm_plan_info": (C.c_int, [_vp, C.c_int, _i64, _vp, _i64, _vp, _i64, C.c_uint, _vp, _vp]),
     "daspmm_debug_conditional_scan_f64": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "daspmm_selected_cache_info": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
 }
 
 _lib = None

@@ -83,19 +83,39 @@ static int pow2_ceil(int64_t x) {
     return p;
 }
 
-// Stream-ordered scratch comes from the device's default memory pool. Keep freed
-// blocks in the pool (the default release threshold of 0 would unmap them at every
-// synchronisation and remap them on the next call).
-static void keep_pool_warm(int dev) {
-    static bool done[64] = {};
-    if (dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// Stream-ordered scratch (EB chunk rows, layout conversions) comes from a memory pool the
+// library owns, one per device, so the host process's default pool keeps its own
+// settings. Up to 256 MB of freed blocks stay reserved between calls, so a steady stream
+// of calls does not unmap and remap its scratch on every synchronisation.
+static cudaMemPool_t lib_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    static bool tried[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!tried[dev]) {
+        tried[dev] = true;
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            pools[dev] = nullptr;
+        } else {
+            uint64_t thr = uint64_t(256) << 20;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
     }
-    done[dev] = true;
+    return pools[dev];
 }
+
+cudaError_t scratch_alloc(void** p, size_t bytes, int dev, cudaStream_t s) {
+    cudaMemPool_t pool = lib_pool(dev);
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
+}
+
+cudaError_t scratch_free(void* p, cudaStream_t s) { return p ? cudaFreeAsync(p, s) : cudaSuccess; }
 
 // Planner tuning knobs (environment, all optional; documented at their uses and in
 // INTEGRATION.md). Read once into a snapshot so the per-call host path does no getenv;
@@ -476,7 +496,6 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
                 int64_t ldb, int64_t N, void* C, int64_t ldc, unsigned flags, cudaStream_t s,
                 int* chunk_scratch) {
     if (h->M == 0 || N == 0) return DASPMM_OK;
-    if (chunk_scratch == nullptr) keep_pool_warm(h->device);  // never inside a graph capture
     const bool exact = (flags & DASPMM_EXACT) != 0;
     const bool own_scratch = chunk_scratch == nullptr;
     // EB kernels and the lean SR kernels read COO row ids (graph bodies get the array
@@ -487,13 +506,14 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     int* chunk_row = chunk_scratch;
     cudaError_t e;
     if (kernel >= 4 && own_scratch) {
-        if ((e = cudaMallocAsync(&chunk_row, sizeof(int) * size_t(std::max<int64_t>(p.P, 1)), s)) !=
+        if ((e = scratch_alloc(reinterpret_cast<void**>(&chunk_row),
+                               sizeof(int) * size_t(std::max<int64_t>(p.P, 1)), h->device, s)) !=
             cudaSuccess)
-            return cuda_fail(e, "cudaMallocAsync(chunk_row)");
+            return cuda_fail(e, "scratch_alloc(chunk_row)");
     }
     e = h->dtype == DASPMM_F64 ? run_plan<double>(h, p, W, B, ldb, N, C, ldc, chunk_row, s)
                                : run_plan<float>(h, p, W, B, ldb, N, C, ldc, chunk_row, s);
-    if (chunk_row && own_scratch) cudaFreeAsync(chunk_row, s);
+    if (chunk_row && own_scratch) scratch_free(chunk_row, s);
     if (e == cudaSuccess && knobs().fault) e = inject_fault(h->dtype, C, s);
     if (e == cudaErrorNotSupported)
         return fail(DASPMM_ERR_UNSUPPORTED, std::string("spmm: no instantiation for kernel ") +
@@ -584,6 +604,55 @@ cudaError_t transpose(int dtype, const void* in, int64_t rows, int64_t cols, int
     return cudaGetLastError();
 }
 
+// Device ingest of a host CSR (types.hpp:56-148): the int64 offsets and columns, as the
+// reference stores them, are uploaded once and one pass validates and compacts them to
+// the device's int32 layout. bad[0] = first i with offsets[i] < offsets[i-1], bad[1] =
+// first element whose column is outside [0, K) (INT64_MAX when none).
+__global__ void k_ingest(const int64_t* __restrict__ rp64, const int64_t* __restrict__ ci64,
+                         int64_t M, int64_t K, int64_t nnz, int32_t* __restrict__ rp32,
+                         int32_t* __restrict__ ci32, unsigned long long* bad) {
+    const int64_t n = M + 1 > nnz ? M + 1 : nnz;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        if (i <= M) {
+            const int64_t v = rp64[i];
+            rp32[i] = int32_t(v);
+            if (i > 0 && v < rp64[i - 1]) atomicMin(bad, (unsigned long long)i);
+        }
+        if (i < nnz) {
+            const int64_t c = ci64[i];
+            ci32[i] = int32_t(c);
+            if (c < 0 || c >= K) atomicMin(bad + 1, (unsigned long long)i);
+        }
+    }
+}
+
+cudaError_t ingest(const int64_t* rp, const int64_t* ci, int64_t M, int64_t K, int64_t nnz,
+                   int32_t* rp32, int32_t* ci32, int64_t bad_out[2]) {
+    int64_t* d64 = nullptr;
+    unsigned long long* d_bad = nullptr;
+    const size_t n_rp = size_t(M) + 1, n_ci = size_t(nnz);
+    cudaError_t e = cudaMalloc(&d64, sizeof(int64_t) * (n_rp + std::max<size_t>(n_ci, 1)));
+    if (e == cudaSuccess) e = cudaMalloc(&d_bad, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(d_bad, 0xff, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemcpy(d64, rp, sizeof(int64_t) * n_rp, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_ci > 0)
+        e = cudaMemcpy(d64 + n_rp, ci, sizeof(int64_t) * n_ci, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const int64_t n = std::max<int64_t>(M + 1, nnz);
+        const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 32));
+        k_ingest<<<blocks, 256>>>(d64, d64 + n_rp, M, K, nnz, rp32, ci32, d_bad);
+        e = cudaGetLastError();
+    }
+    unsigned long long hb[2] = {~0ull, ~0ull};
+    if (e == cudaSuccess) e = cudaMemcpy(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost);
+    cudaFree(d64);
+    cudaFree(d_bad);
+    for (int i = 0; i < 2; ++i)
+        bad_out[i] = hb[i] == ~0ull ? INT64_MAX : int64_t(hb[i]);
+    return e;
+}
+
 }  // namespace daspmm
 
 using namespace daspmm;
@@ -623,23 +692,10 @@ int daspmm_csr_create_host(int64_t M, int64_t K, int64_t nnz, const int64_t* rp,
         return fail(DASPMM_ERR_UNSUPPORTED, "csr_create: sizes must be < 2^31 - 1 (int32 device CSR)");
     if (!rp || (nnz > 0 && (!ci || !values)))
         return fail(DASPMM_ERR_INVALID_ARG, "csr_create: null array");
-    // types.hpp:96-148 invariants the kernels depend on.
+    // types.hpp:96-148 invariants the kernels depend on. The O(1) ends are checked here;
+    // monotonicity and the column bounds are checked on the device by the same pass
+    // that compacts the int64 arrays to int32 (k_ingest); messages keep this order.
     if (rp[0] != 0) return fail(DASPMM_ERR_INVALID_ARG, "csr_create: row_offsets[0] != 0");
-    for (int64_t i = 1; i <= M; ++i)
-        if (rp[i] < rp[i - 1])
-            return fail(DASPMM_ERR_INVALID_ARG,
-                        "csr_create: row_offsets nondecreasing violated at index " + std::to_string(i));
-    if (rp[M] != nnz)
-        return fail(DASPMM_ERR_INVALID_ARG, "csr_create: row_offsets[num_rows] != nnz");
-    std::vector<int32_t> rp32(static_cast<size_t>(M) + 1);
-    std::vector<int32_t> ci32(static_cast<size_t>(nnz));
-    for (int64_t i = 0; i <= M; ++i) rp32[i] = int32_t(rp[i]);
-    for (int64_t i = 0; i < nnz; ++i) {
-        if (ci[i] < 0 || ci[i] >= K)
-            return fail(DASPMM_ERR_INVALID_ARG,
-                        "csr_create: col index bound violated at index " + std::to_string(i));
-        ci32[i] = int32_t(ci[i]);
-    }
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || daspmm_device_count() == 0) {
         cudaGetLastError();
@@ -659,14 +715,22 @@ int daspmm_csr_create_host(int64_t M, int64_t K, int64_t nnz, const int64_t* rp,
         daspmm_csr_destroy(h);
         return cuda_fail(e, "csr_create: cudaMalloc");
     }
-    cudaMemcpy(h->rp, rp32.data(), sizeof(int32_t) * (M + 1), cudaMemcpyHostToDevice);
-    if (nnz > 0) {
-        cudaMemcpy(h->ci, ci32.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
-        cudaMemcpy(h->va, values, es * nnz, cudaMemcpyHostToDevice);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) {
+    int64_t bad[2] = {INT64_MAX, INT64_MAX};
+    if ((e = ingest(rp, ci, M, K, nnz, h->rp, h->ci, bad)) != cudaSuccess ||
+        (nnz > 0 && (e = cudaMemcpy(h->va, values, es * nnz, cudaMemcpyHostToDevice)) != cudaSuccess)) {
         daspmm_csr_destroy(h);
         return cuda_fail(e, "csr_create: upload");
+    }
+    std::string msg;
+    if (bad[0] != INT64_MAX)
+        msg = "csr_create: row_offsets nondecreasing violated at index " + std::to_string(bad[0]);
+    else if (rp[M] != nnz)
+        msg = "csr_create: row_offsets[num_rows] != nnz";
+    else if (bad[1] != INT64_MAX)
+        msg = "csr_create: col index bound violated at index " + std::to_string(bad[1]);
+    if (!msg.empty()) {
+        daspmm_csr_destroy(h);
+        return fail(DASPMM_ERR_INVALID_ARG, msg);
     }
     return finish_create(h, 0, out);
 }
@@ -817,8 +881,10 @@ int daspmm_spmm_host(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int6
         cudaFree(dB);
         return cuda_fail(e, "spmm_host: cudaMalloc(C)");
     }
-    cudaMemcpy(dB, B, bbytes, cudaMemcpyHostToDevice);
-    int rc = spmm_device(h, kernel, P, W, dB, ldb, N, dC, N, flags, 0, nullptr);
+    int rc = DASPMM_OK;
+    if ((e = cudaMemcpy(dB, B, bbytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+        rc = cuda_fail(e, "spmm_host: upload B");
+    if (rc == DASPMM_OK) rc = spmm_device(h, kernel, P, W, dB, ldb, N, dC, N, flags, 0, nullptr);
     if (rc == DASPMM_OK) {
         e = cudaMemcpy(C, dC, cbytes, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) rc = cuda_fail(e, "spmm_host");
@@ -844,8 +910,8 @@ int daspmm_spmm_auto_layout(const daspmm_csr* h, int kernel, int64_t P, int64_t 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t es = size_t(elem_size(h->dtype));
     void* t = nullptr;
-    cudaError_t e = cudaMallocAsync(&t, std::max<size_t>(es * size_t(h->K) * size_t(N), 16), s);
-    if (e != cudaSuccess) return cuda_fail(e, "spmm_auto_layout: cudaMallocAsync");
+    cudaError_t e = scratch_alloc(&t, std::max<size_t>(es * size_t(h->K) * size_t(N), 16), h->device, s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm_auto_layout: scratch_alloc");
     int64_t ldt;
     if (b_layout == DASPMM_ROW_MAJOR) {  // K x N (ldb) -> ColMajor: N x K rows, ld K
         ldt = std::max<int64_t>(h->K, 1);
@@ -857,7 +923,7 @@ int daspmm_spmm_auto_layout(const daspmm_csr* h, int kernel, int64_t P, int64_t 
     int rc = e == cudaSuccess ? daspmm_spmm(h, kernel, P, W, Cb, t, want, ldt, N, d_C, ldc, flags,
                                             stream)
                               : cuda_fail(e, "spmm_auto_layout: transpose");
-    cudaFreeAsync(t, s);
+    scratch_free(t, s);
     return rc;
 }
 
@@ -922,13 +988,13 @@ int daspmm_spmm_rows_to(const daspmm_csr* h, const void* B, int64_t ldb, int64_t
     if (h->M == 0 || N == 0) return DASPMM_OK;
     DeviceGuard g(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    keep_pool_warm(h->device);
     // RB+RM+SR through the shuffle-broadcast row walk (k_rb_sr): every row is owned by
     // exactly one group, so the replicated epilogue needs plain stores only. The vector
     // width must suit every destination, so the plan checks the least aligned one.
-    const void* worst = C[0];
-    for (int d = 1; d < n_dst; ++d)
-        if ((reinterpret_cast<uintptr_t>(C[d]) & 15) != 0) worst = C[d];
+    // OR of all destination addresses: its lowest set bit is the minimum alignment.
+    uintptr_t any = 0;
+    for (int d = 0; d < n_dst; ++d) any |= reinterpret_cast<uintptr_t>(C[d]);
+    const void* worst = reinterpret_cast<const void*>(any);
     Plan p = plan_spmm(h, 0, 0, 8, N, B, ldb, worst, ldc, false, /*base_only=*/true);
     p.repl = true;
     cudaError_t e = run_plan<float>(h, p, 8, B, ldb, N, C[0], ldc, nullptr, s, C + 1, n_dst - 1);
@@ -942,6 +1008,7 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
                      const void* C, int64_t ldc, unsigned flags, int* variant, int64_t* param) {
     if (!h || !variant || !param) return fail(DASPMM_ERR_INVALID_ARG, "plan_info: null argument");
     if (kernel < 0 || kernel > 7) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
+    DeviceGuard g(h->device);
     if (int rc = ensure_coo(h, 0)) return rc;
     const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
     *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
@@ -954,9 +1021,14 @@ int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out) {
     if (w < 1 || w > 32 || !is_pow2(w))
         return fail(DASPMM_ERR_INVALID_ARG, "tree_reduce: length must be a power of two <= 32");
     double *d_in = nullptr, *d_out = nullptr;
-    cudaMalloc(&d_in, sizeof(double) * 32);
-    cudaMalloc(&d_out, sizeof(double));
-    cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice);
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_in, sizeof(double) * 32)) != cudaSuccess ||
+        (e = cudaMalloc(&d_out, sizeof(double))) != cudaSuccess ||
+        (e = cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(d_in);
+        cudaFree(d_out);
+        return cuda_fail(e, "debug_tree_reduce");
+    }
     switch (w) {
         case 1: k_debug_tree<1><<<1, 32>>>(d_in, d_out, int(w)); break;
         case 2: k_debug_tree<2><<<1, 32>>>(d_in, d_out, int(w)); break;
@@ -965,7 +1037,7 @@ int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out) {
         case 16: k_debug_tree<16><<<1, 32>>>(d_in, d_out, int(w)); break;
         default: k_debug_tree<32><<<1, 32>>>(d_in, d_out, int(w)); break;
     }
-    cudaError_t e = cudaMemcpy(out, d_out, sizeof(double), cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(out, d_out, sizeof(double), cudaMemcpyDeviceToHost);
     cudaFree(d_in);
     cudaFree(d_out);
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "debug_tree_reduce");
@@ -977,13 +1049,19 @@ int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, 
         return fail(DASPMM_ERR_INVALID_ARG, "conditional_scan: length must be a power of two <= 32");
     double *d_in = nullptr, *d_out = nullptr;
     int64_t* d_ids = nullptr;
-    cudaMalloc(&d_in, sizeof(double) * 32);
-    cudaMalloc(&d_out, sizeof(double) * 32);
-    cudaMalloc(&d_ids, sizeof(int64_t) * 32);
-    cudaMemset(d_in, 0, sizeof(double) * 32);
-    cudaMemset(d_ids, 0xff, sizeof(int64_t) * 32);
-    cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice);
-    cudaMemcpy(d_ids, ids, sizeof(int64_t) * w, cudaMemcpyHostToDevice);
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_in, sizeof(double) * 32)) != cudaSuccess ||
+        (e = cudaMalloc(&d_out, sizeof(double) * 32)) != cudaSuccess ||
+        (e = cudaMalloc(&d_ids, sizeof(int64_t) * 32)) != cudaSuccess ||
+        (e = cudaMemset(d_in, 0, sizeof(double) * 32)) != cudaSuccess ||
+        (e = cudaMemset(d_ids, 0xff, sizeof(int64_t) * 32)) != cudaSuccess ||
+        (e = cudaMemcpy(d_in, values, sizeof(double) * w, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(d_ids, ids, sizeof(int64_t) * w, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(d_in);
+        cudaFree(d_out);
+        cudaFree(d_ids);
+        return cuda_fail(e, "debug_conditional_scan");
+    }
     switch (w) {
         case 1: k_debug_cond<1><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
         case 2: k_debug_cond<2><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
@@ -992,7 +1070,7 @@ int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, 
         case 16: k_debug_cond<16><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
         default: k_debug_cond<32><<<1, 32>>>(d_in, d_ids, d_out, int(w)); break;
     }
-    cudaError_t e = cudaMemcpy(out, d_out, sizeof(double) * w, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(out, d_out, sizeof(double) * w, cudaMemcpyDeviceToHost);
     cudaFree(d_in);
     cudaFree(d_out);
     cudaFree(d_ids);

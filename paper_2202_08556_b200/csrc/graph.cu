@@ -8,6 +8,7 @@
 // does, spmm.hpp:275-281). The host never learns the choice — no round trip — and a
 // repeated call is a single cudaGraphLaunch.
 #include <cstring>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -20,6 +21,7 @@ namespace daspmm {
 
 namespace {
 
+// Graph entries: the full operand key (the captured kernels bake in B, C and the stream).
 struct Key {
     uint64_t model_gen;
     const void* B;
@@ -29,16 +31,27 @@ struct Key {
     int64_t ldc, W;
     unsigned flags;
     int64_t hw;
-    int* d_kernel;
     cudaStream_t stream;
-    bool operator<(const Key& o) const {
-        return std::tie(model_gen, B, b_layout, ldb, N, C, ldc, W, flags, hw, d_kernel, stream) <
+    bool operator==(const Key& o) const {
+        return std::tie(model_gen, B, b_layout, ldb, N, C, ldc, W, flags, hw, stream) ==
                std::tie(o.model_gen, o.B, o.b_layout, o.ldb, o.N, o.C, o.ldc, o.W, o.flags, o.hw,
-                        o.d_kernel, o.stream);
+                        o.stream);
+    }
+};
+
+// The selector's choice is a pure function of (matrix, model, N, hw) — operands never
+// enter it — so once the device has published it, every later call with that key
+// (any B, C, stream) launches the chosen kernel directly.
+struct DecisionKey {
+    uint64_t model_gen;
+    int64_t N, hw;
+    bool operator<(const DecisionKey& o) const {
+        return std::tie(model_gen, N, hw) < std::tie(o.model_gen, o.N, o.hw);
     }
 };
 
 struct Entry {
+    Key key{};
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int* chunk_row = nullptr;
@@ -46,12 +59,12 @@ struct Entry {
     int* own_kernel = nullptr;
     int* decision = nullptr;  // device cache of the selector's choice (-1 = not yet made)
     // The selector kernel also publishes its choice into mapped pinned host memory.
-    // Once it is visible, later identical calls launch the chosen kernel directly —
-    // the device made the decision; the host never waits for it.
     int* published = nullptr;        // host view
     int* published_dev = nullptr;    // device view
-    const void* Bk = nullptr;        // per-kernel operand for the direct path
+    cudaEvent_t done = nullptr;      // recorded after the entry's last launch
     ~Entry() {
+        // cudaGraphExecDestroy defers the release of an in-flight graph; the scratch
+        // below is only freed once `done` has completed (retire / graph_cache_free).
         cudaFree(decision);
         if (published) cudaFreeHost(published);
         if (exec) cudaGraphExecDestroy(exec);
@@ -59,15 +72,62 @@ struct Entry {
         cudaFree(chunk_row);
         cudaFree(bt);
         cudaFree(own_kernel);
+        if (done) cudaEventDestroy(done);
     }
+    bool idle() const { return done == nullptr || cudaEventQuery(done) != cudaErrorNotReady; }
 };
+
+// At most kMaxGraphs instantiated graphs per handle (LRU); an evicted or decided entry is
+// retired and freed once its last launch has completed.
+constexpr size_t kMaxGraphs = 4;
 
 struct Cache {
     std::mutex mu;
-    std::map<Key, std::unique_ptr<Entry>> entries;
+    std::map<DecisionKey, int> decided;
+    std::list<std::unique_ptr<Entry>> lru;      // front = most recently used
+    std::vector<std::unique_ptr<Entry>> retired;
+
+    void reap() {
+        for (size_t i = 0; i < retired.size();) {
+            if (retired[i]->idle()) {
+                retired[i] = std::move(retired.back());
+                retired.pop_back();
+            } else {
+                ++i;
+            }
+        }
+        cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+    }
+    void retire(std::list<std::unique_ptr<Entry>>::iterator it) {
+        retired.push_back(std::move(*it));
+        lru.erase(it);
+    }
+    ~Cache() {
+        for (auto& e : lru)
+            if (e->done) cudaEventSynchronize(e->done);
+        for (auto& e : retired)
+            if (e->done) cudaEventSynchronize(e->done);
+    }
 };
 
 int elem(int dtype) { return dtype == DASPMM_F64 ? 8 : 4; }
+
+// Kernel ids 0..7 in pinned host memory: the direct path writes the caller's d_kernel
+// with an async copy from here (a pageable source would serialise the stream).
+const int* pinned_ids() {
+    static int* ids = [] {
+        int* p = nullptr;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&p), 8 * sizeof(int), cudaHostAllocDefault) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            static int fallback[8];
+            p = fallback;
+        }
+        for (int i = 0; i < 8; ++i) p[i] = i;
+        return p;
+    }();
+    return ids;
+}
 
 }  // namespace
 
@@ -76,14 +136,30 @@ void graph_cache_free(daspmm_csr* h) {
     h->graph_cache = nullptr;
 }
 
-static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k, Entry& en) {
-    cudaError_t e;
-    int* d_kernel = k.d_kernel;
-    if (!d_kernel) {
-        if ((e = cudaMalloc(&en.own_kernel, sizeof(int))) != cudaSuccess)
-            return cuda_fail(e, "graph: cudaMalloc");
-        d_kernel = en.own_kernel;
+static int graph_cache_stats(const daspmm_csr* h, int64_t* graphs, int64_t* retired, int64_t* decided) {
+    Cache* c = static_cast<Cache*>(h->graph_cache);
+    int64_t g = 0, r = 0, d = 0;
+    if (c) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->reap();
+        g = int64_t(c->lru.size());
+        r = int64_t(c->retired.size());
+        d = int64_t(c->decided.size());
     }
+    if (graphs) *graphs = g;
+    if (retired) *retired = r;
+    if (decided) *decided = d;
+    return DASPMM_OK;
+}
+
+static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k, bool reselect,
+                       Entry& en) {
+    cudaError_t e;
+    en.key = k;
+    if ((e = cudaMalloc(&en.own_kernel, sizeof(int))) != cudaSuccess)
+        return cuda_fail(e, "graph: cudaMalloc");
+    if ((e = cudaEventCreateWithFlags(&en.done, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "graph: event");
     if (int rc = ensure_coo(h, 0)) return rc;  // EB bodies read COO row ids
     // Scratch: EB chunk rows for the largest plan, and B in the other layout.
     int64_t max_p = 1;
@@ -131,8 +207,10 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     if ((e = cudaStreamBeginCaptureToGraph(cap, en.graph, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return cuda_fail(e, "graph: capture(select)");
-    int rc = launch_select(h, m, k.N, k.hw, d_kernel, cond, true, cap, en.decision,
-                           en.published_dev);
+    // reselect (DASPMM_RESELECT): no device-side decision cache and no publication, so
+    // every launch walks the ensemble and dispatches through the SWITCH node.
+    int rc = launch_select(h, m, k.N, k.hw, en.own_kernel, cond, true, cap,
+                           reselect ? nullptr : en.decision, reselect ? nullptr : en.published_dev);
     cudaGraph_t g_out = nullptr;
     e = cudaStreamEndCapture(cap, &g_out);
     if (rc) return rc;
@@ -208,6 +286,9 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
         return fail(DASPMM_ERR_INVALID_ARG,
                     "encode_features: model expects a hardware_id but the sample has none");
     if (nf != (uh ? 5 : 4)) return fail(DASPMM_ERR_INVALID_ARG, "predict: feature count mismatch");
+    // The SWITCH node has eight bodies; KernelId::from_index rejects any other class
+    // (kernel_id.hpp:30), so a model that could predict one is refused up front.
+    if (nc > 8) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
     if (N == 0) return DASPMM_OK;
     DeviceGuard g(h->device);
     daspmm_csr* hm = const_cast<daspmm_csr*>(h);
@@ -216,43 +297,87 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
         if (!hm->graph_cache) hm->graph_cache = new Cache;
     }
     Cache* cache = static_cast<Cache*>(hm->graph_cache);
-    const Key key{model_generation(m), d_B, b_layout, ldb, N, d_C, ldc, W, flags, uh ? hw : -1,
-                  d_kernel, static_cast<cudaStream_t>(stream)};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool reselect = (flags & DASPMM_RESELECT) != 0;
+    const unsigned kflags = flags & ~unsigned(DASPMM_RESELECT);
+    const DecisionKey dk{model_generation(m), N, uh ? hw : -1};
+    const Key key{model_generation(m), d_B, b_layout, ldb, N, d_C, ldc, W, kflags, uh ? hw : -1, s};
+
+    int decided = -1;
     Entry* en = nullptr;
     {
         std::lock_guard<std::mutex> lk(cache->mu);
-        auto it = cache->entries.find(key);
-        if (it == cache->entries.end()) {
-            auto fresh = std::make_unique<Entry>();
-            if (int rc = build_entry(h, m, key, *fresh)) {
-                // A graph left mid-capture cannot be destroyed safely; leak it.
-                fresh->graph = nullptr;
-                return rc;
+        // Entries whose selector has published: record the decision, retire the graph.
+        for (auto it = cache->lru.begin(); it != cache->lru.end();) {
+            const int pub = *reinterpret_cast<volatile int*>((*it)->published);
+            if (pub >= 0 && pub < 8) {
+                cache->decided[DecisionKey{(*it)->key.model_gen, (*it)->key.N, (*it)->key.hw}] = pub;
+                auto nx = std::next(it);
+                cache->retire(it);
+                it = nx;
+            } else {
+                ++it;
             }
-            it = cache->entries.emplace(key, std::move(fresh)).first;
         }
-        en = it->second.get();
-    }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int decided = *reinterpret_cast<volatile int*>(en->published);
-    if (decided >= 0 && decided < 8) {
-        // Steady state: the device's published choice, launched directly (same plan
-        // and scratch as the SWITCH body).
-        const int want = ((decided >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
-        if (want == b_layout)
-            return spmm_device(h, decided, 0, W, d_B, ldb, N, d_C, ldc, flags, s, en->chunk_row);
-        if (en->bt) {
-            const int64_t ldt = b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
-                                                             : std::max<int64_t>(N, 1);
-            cudaError_t e = b_layout == DASPMM_ROW_MAJOR
-                                ? transpose(h->dtype, d_B, h->K, N, ldb, en->bt, ldt, s)
-                                : transpose(h->dtype, d_B, N, h->K, ldb, en->bt, ldt, s);
-            if (e != cudaSuccess) return cuda_fail(e, "transpose");
-            return spmm_device(h, decided, 0, W, en->bt, ldt, N, d_C, ldc, flags, s,
-                               en->chunk_row);
+        if (!reselect) {
+            auto d = cache->decided.find(dk);
+            if (d != cache->decided.end()) decided = d->second;
         }
-        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, flags, s, en->chunk_row);
+        if (decided < 0) {
+            for (auto it = cache->lru.begin(); it != cache->lru.end(); ++it) {
+                if ((*it)->key == key) {
+                    cache->lru.splice(cache->lru.begin(), cache->lru, it);
+                    en = cache->lru.front().get();
+                    break;
+                }
+            }
+            if (!en) {
+                // Freeing retired graphs synchronises (cudaFree, cudaFreeHost), so it is
+                // done only here, on the already slow build path — never on a launch.
+                cache->reap();
+                auto fresh = std::make_unique<Entry>();
+                if (int rc = build_entry(h, m, key, reselect, *fresh)) {
+                    // A graph left mid-capture cannot be destroyed safely; leak it.
+                    fresh->graph = nullptr;
+                    return rc;
+                }
+                cache->lru.push_front(std::move(fresh));
+                en = cache->lru.front().get();
+                while (cache->lru.size() > kMaxGraphs) cache->retire(std::prev(cache->lru.end()));
+            }
+            cudaError_t e = cudaGraphLaunch(en->exec, s);
+            if (e == cudaSuccess) e = cudaEventRecord(en->done, s);
+            if (e == cudaSuccess && d_kernel)
+                e = cudaMemcpyAsync(d_kernel, en->own_kernel, sizeof(int), cudaMemcpyDeviceToDevice, s);
+            return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "graph launch");
+        }
     }
-    cudaError_t e = cudaGraphLaunch(en->exec, s);
-    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "graph launch");
+    // Steady state: the device's published choice, launched directly. Scratch (EB chunk
+    // rows, B in the other layout) is stream-ordered from the library pool.
+    cudaError_t e = cudaSuccess;
+    if (d_kernel)
+        e = cudaMemcpyAsync(d_kernel, pinned_ids() + decided, sizeof(int), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm_selected: kernel id");
+    const int want = ((decided >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
+    if (want == b_layout) return spmm_device(h, decided, 0, W, d_B, ldb, N, d_C, ldc, kflags, s, nullptr);
+    const size_t bytes = size_t(elem(h->dtype)) * size_t(h->K) * size_t(N);
+    void* bt = nullptr;
+    if (scratch_alloc(&bt, std::max<size_t>(bytes, 16), h->device, s) != cudaSuccess) {
+        cudaGetLastError();  // no room for the other layout: the layout twin (same M/K choices)
+        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, kflags, s, nullptr);
+    }
+    const int64_t ldt = b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
+                                                     : std::max<int64_t>(N, 1);
+    e = b_layout == DASPMM_ROW_MAJOR ? transpose(h->dtype, d_B, h->K, N, ldb, bt, ldt, s)
+                                     : transpose(h->dtype, d_B, N, h->K, ldb, bt, ldt, s);
+    int rc = e == cudaSuccess ? spmm_device(h, decided, 0, W, bt, ldt, N, d_C, ldc, kflags, s, nullptr)
+                              : cuda_fail(e, "transpose");
+    scratch_free(bt, s);
+    return rc;
+}
+
+extern "C" int daspmm_selected_cache_info(const daspmm_csr* h, int64_t* graphs, int64_t* retired,
+                                          int64_t* decided) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "selected_cache_info: null handle");
+    return graph_cache_stats(h, graphs, retired, decided);
 }

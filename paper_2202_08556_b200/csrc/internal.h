@@ -85,6 +85,9 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
                 int* chunk_scratch);
 int check_call(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t Cb, int b_layout,
                int64_t ldb, int64_t N, int64_t ldc, bool exact);
+// Stream-ordered scratch from the library's own per-device memory pool.
+cudaError_t scratch_alloc(void** p, size_t bytes, int dev, cudaStream_t s);
+cudaError_t scratch_free(void* p, cudaStream_t s);
 cudaError_t transpose(int dtype, const void* in, int64_t rows, int64_t cols, int64_t ldi,
                       void* out, int64_t ldo, cudaStream_t s);
 // Implemented in select.cu

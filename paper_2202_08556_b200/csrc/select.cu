@@ -211,9 +211,12 @@ int parse_model(const char* text, size_t len, daspmm_model** out) {
         if ((e = cudaMalloc(&m->d_nodes, sizeof(DevNode) * nodes.size())) != cudaSuccess ||
             (e = cudaMalloc(&m->d_tree_off, sizeof(int64_t) * m->tree_off.size())) != cudaSuccess)
             return cuda_fail(e, "model upload");
-        cudaMemcpy(m->d_nodes, nodes.data(), sizeof(DevNode) * nodes.size(), cudaMemcpyHostToDevice);
-        cudaMemcpy(m->d_tree_off, m->tree_off.data(), sizeof(int64_t) * m->tree_off.size(),
-                   cudaMemcpyHostToDevice);
+        if ((e = cudaMemcpy(m->d_nodes, nodes.data(), sizeof(DevNode) * nodes.size(),
+                            cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(m->d_tree_off, m->tree_off.data(),
+                            sizeof(int64_t) * m->tree_off.size(), cudaMemcpyHostToDevice)) !=
+                cudaSuccess)
+            return cuda_fail(e, "model upload");
     }
     *out = guard.release();
     return DASPMM_OK;
@@ -430,6 +433,7 @@ int daspmm_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, in
         return fail(DASPMM_ERR_INVALID_ARG, "predict: feature count mismatch");
     if (h->M == 0)
         return fail(DASPMM_ERR_INVALID_ARG, "extract_features: matrix has no rows to summarize");
+    if (m->num_classes > 8) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
     if (!m->d_nodes) return fail(DASPMM_ERR_CUDA, "select: model not resident on a device");
     DeviceGuard g(h->device);
     return launch_select(h, m, n_cols, hw, d_kernel, cudaGraphConditionalHandle{}, false,

@@ -58,12 +58,21 @@ class GCNGraph:
         path = model_path or os.path.join(os.path.dirname(__file__), "models",
                                           "b200_selector.txt")
         self.model = sk.load_selector(open(path).read())
+        self._out = {}  # (N, dtype) -> the graph's own output buffer
 
     def aggregate(self, H: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """Â · H (row-major fp32, N = H.shape[1] columns) through DA-SpMM."""
+        """Â · H (row-major fp32, N = H.shape[1] columns) through DA-SpMM.
+
+        Without ``out`` the result lands in a buffer the graph owns (one per width and
+        dtype), which the next aggregate of the same width overwrites — clone it to keep
+        it. Layer after layer thus allocates nothing on the SpMM side."""
         H = H.contiguous()
         if out is None:
-            out = torch.empty(self.num_nodes, H.shape[1], device=H.device, dtype=H.dtype)
+            key = (H.shape[1], H.dtype)
+            out = self._out.get(key)
+            if out is None or out.device != H.device:
+                out = torch.empty(self.num_nodes, H.shape[1], device=H.device, dtype=H.dtype)
+                self._out[key] = out
         sk.spmm_selected(self.adj, self.model, H, out)
         return out
 

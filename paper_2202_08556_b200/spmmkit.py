@@ -240,10 +240,11 @@ def _dtype_code(dtype) -> int:
 class DeviceCsr:
     """Device-resident CSR handle (int32 offsets/cols on the GPU)."""
 
-    def __init__(self, handle: int, dtype, keepalive=None):
+    def __init__(self, handle: int, dtype, keepalive=None, device: Optional[int] = None):
         self._h = C.c_void_p(handle)
         self.dtype = np.dtype(dtype)
         self._keep = keepalive
+        self.device = _current_device() if device is None else int(device)
         M, K, nnz, dt, ne, ct = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int(), C.c_int64(),
                                  C.c_int64())
         check(lib().daspmm_csr_info(self._h, C.byref(M), C.byref(K), C.byref(nnz), C.byref(dt),
@@ -277,12 +278,12 @@ class DeviceCsr:
                                              values.data_ptr(), _dtype_code(dtype), int(copy),
                                              _stream_ptr(stream), C.byref(out)))
         keep = None if copy else (row_offsets, col_indices, values)
-        return DeviceCsr(out.value, dtype, keep)
+        return DeviceCsr(out.value, dtype, keep, row_offsets.device.index)
 
     def panel(self, r0: int, r1: int, stream=None) -> "DeviceCsr":
         out = C.c_void_p()
         check(lib().daspmm_csr_create_panel(self._h, r0, r1, _stream_ptr(stream), C.byref(out)))
-        return DeviceCsr(out.value, self.dtype)
+        return DeviceCsr(out.value, self.dtype, device=self.device)
 
     def nnz(self) -> int:
         return self._nnz
@@ -302,6 +303,49 @@ class DeviceCsr:
             self.close()
         except Exception:
             pass
+
+
+def _current_device() -> int:
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return 0
+
+
+_TORCH_DT = {np.dtype(np.float32): "torch.float32", np.dtype(np.float64): "torch.float64"}
+
+
+def _check_operands(a: DeviceCsr, B, C_out, b_layout, what: str = "spmm"):
+    """The checks the C ABI cannot make on raw pointers (spmm.hpp:197-209 for the
+    dimensions): 2-D CUDA tensors on the handle's device, the handle's value type,
+    unit column stride, B with K rows (K x N row-major, or the N x K buffer of a
+    column-major B) and C of M x N."""
+    for name, t in (("B", B), ("C", C_out)):
+        if getattr(t, "dim", lambda: -1)() != 2:
+            raise InvalidArgument(_lib.ERR_INVALID_ARG, f"{what}: {name} must be a 2-D tensor")
+        if not t.is_cuda or t.device.index != a.device:
+            raise InvalidArgument(_lib.ERR_INVALID_ARG,
+                                  f"{what}: {name} must be a CUDA tensor on cuda:{a.device}, "
+                                  f"got {t.device}")
+        if str(t.dtype) != _TORCH_DT.get(a.dtype):
+            raise InvalidArgument(_lib.ERR_INVALID_ARG,
+                                  f"{what}: {name} is {t.dtype} but A holds {a.dtype}")
+        if t.shape[1] > 1 and t.stride(1) != 1:
+            raise InvalidArgument(_lib.ERR_INVALID_ARG,
+                                  f"{what}: {name} needs unit column stride, got {t.stride(1)}")
+    k_rows = B.shape[0] if b_layout == Layout.RowMajor else B.shape[1]
+    n = B.shape[1] if b_layout == Layout.RowMajor else B.shape[0]
+    if k_rows != a.num_cols:
+        raise InvalidArgument(_lib.ERR_DIMS, f"{what}: A is {a.num_rows}x{a.num_cols} but X has "
+                                             f"{k_rows} rows")
+    if tuple(C_out.shape) != (a.num_rows, n):
+        raise InvalidArgument(_lib.ERR_DIMS, f"{what}: C is {C_out.shape[0]}x{C_out.shape[1]}, "
+                                             f"expected {a.num_rows}x{n}")
+    return n
 
 
 def _stream_ptr(stream):
@@ -372,7 +416,7 @@ def spmm_device(kernel, a: DeviceCsr, B, C_out, P: int = 0, W: int = 8, Cb: int 
     kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
     if b_layout is None:
         b_layout = Layout.ColMajor if (kid >> 1) & 1 else Layout.RowMajor
-    n = B.shape[1] if b_layout == Layout.RowMajor else B.shape[0]
+    n = _check_operands(a, B, C_out, b_layout)
     check(lib().daspmm_spmm(a._h, kid, P, W, Cb, B.data_ptr(), int(b_layout), _ld(B), n,
                             C_out.data_ptr(), _ld(C_out), _lib.EXACT if exact else 0,
                             _stream_ptr(stream)))
@@ -383,6 +427,8 @@ def spmm_rows_to(a: DeviceCsr, B, outs, stream=None):
     """RB+RM+SR with the row epilogue replicated into every tensor of `outs` (each
     M x N row-major with the same leading dimension, fp32) — see daspmm_spmm_rows_to."""
     outs = list(outs)
+    for o in outs:
+        _check_operands(a, B, o, Layout.RowMajor, "spmm_rows_to")
     ldc = _ld(outs[0])
     if any(_ld(o) != ldc or tuple(o.shape) != tuple(outs[0].shape) for o in outs):
         raise InvalidArgument(_lib.ERR_DIMS, "spmm_rows_to: destinations differ in shape")
@@ -404,6 +450,7 @@ def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False):
     """(variant name, parameter) of the launch daspmm_spmm would run for these
     row-major device operands — diagnostics (see daspmm_plan_info)."""
     kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
+    _check_operands(a, B, C_out, Layout.RowMajor, "plan_info")
     v, prm = C.c_int(), C.c_int64()
     check(lib().daspmm_plan_info(a._h, kid, B.shape[1], B.data_ptr(), _ld(B), C_out.data_ptr(),
                                  _ld(C_out), _lib.EXACT if exact else 0, C.byref(v),
@@ -492,14 +539,29 @@ def select_device(a: DeviceCsr, model: SelectorModel, n_cols: int, out, hw: int 
 
 
 def spmm_selected(a: DeviceCsr, model: SelectorModel, B, C_out, b_layout=Layout.RowMajor,
-                  W: int = 8, hw: int = -1, exact: bool = False, kernel_out=None, stream=None):
-    """DA-SpMM: device selector + on-device dispatch (graph SWITCH node)."""
-    n = B.shape[1] if b_layout == Layout.RowMajor else B.shape[0]
+                  W: int = 8, hw: int = -1, exact: bool = False, kernel_out=None, stream=None,
+                  reselect: bool = False):
+    """DA-SpMM: device selector + on-device dispatch (graph SWITCH node). Once the
+    device has published its choice for (matrix, model, N, hw), calls launch the chosen
+    kernel directly; ``reselect`` forces the selector + SWITCH path on this call."""
+    b_layout = Layout(b_layout)
+    n = _check_operands(a, B, C_out, b_layout, "spmm_selected")
+    if kernel_out is not None and (not kernel_out.is_cuda or str(kernel_out.dtype) != "torch.int32"):
+        raise InvalidArgument(_lib.ERR_INVALID_ARG, "spmm_selected: kernel_out must be a CUDA int32 tensor")
     kp = kernel_out.data_ptr() if kernel_out is not None else None
+    flags = (_lib.EXACT if exact else 0) | (_lib.RESELECT if reselect else 0)
     check(lib().daspmm_spmm_selected(a._h, model._m, hw, B.data_ptr(), int(b_layout), _ld(B), n,
-                                     C_out.data_ptr(), _ld(C_out), W,
-                                     _lib.EXACT if exact else 0, kp, _stream_ptr(stream)))
+                                     C_out.data_ptr(), _ld(C_out), W, flags, kp,
+                                     _stream_ptr(stream)))
     return C_out
+
+
+def selected_cache_info(a: DeviceCsr):
+    """(instantiated graphs, retired graphs awaiting completion, known decisions) of the
+    handle's DA-SpMM cache (daspmm_selected_cache_info)."""
+    g, r, d = C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib().daspmm_selected_cache_info(a._h, C.byref(g), C.byref(r), C.byref(d)))
+    return g.value, r.value, d.value
 
 
 # ------------------------------------------------------------------ tolerance

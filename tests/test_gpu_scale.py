@@ -1,0 +1,238 @@
+"""GPU parity at the BASELINE.json configurations, full size.
+
+Every check is row-sampled (and for c5 also column-sampled) against the fp64 oracle on the
+sampled sub-problem (oracle/sampled.py): rows of C depend only on rows of A and columns
+of C only on columns of B (spmm.hpp:16-32), so a sample is checked exactly, with the
+order-independent bound |y - y64| <= 2 gamma(len+1) sum|a x| (fp32, u = 2^-24).
+The samples always include rows that straddle EB chunk / CTA-tile boundaries (the rows
+that take atomics) and the first/last non-empty rows.
+
+  * the suite (configs[1]): every (matrix, N) through DA-SpMM (device selector + dispatch);
+    the device's choice equals the host predict_kernel at scale;
+  * every launch variant of plan_spmm forced at scale, asserting that the
+    planner really ran that variant (daspmm_plan_info);
+  * c1 (configs[0]) against the reference's own spmm() from oracle/_ref, exact mode:
+    RB kernels bit-identical, EB kernels bit-identical on rows owned by one chunk;
+  * c3 / c4 row-sampled, c5 row x column sampled.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle import sampled as S
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+    from paper_2202_08556_b200 import gen
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    sk.lib()
+    model = sk.load_selector(open(os.path.join(ROOT, "paper_2202_08556_b200", "models",
+                                               "b200_selector.txt")).read())
+    return torch, gen, sk, model
+
+
+_MATS = {}
+
+
+def _matrix(env, workload, name):
+    """(name, M, K, rp, ci, va, handle, rp_host), generated once per module."""
+    torch, gen, sk, _ = env
+    key = (workload, name)
+    if key not in _MATS:
+        if len(_MATS) >= 3:  # bound device memory: keep the three most recent
+            _MATS.pop(next(iter(_MATS)))
+            torch.cuda.empty_cache()
+        for nm, mk, ns in gen.workload(workload):
+            if nm == name:
+                M, K, rp, ci, va = mk()
+                d = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+                _MATS[key] = (M, K, rp, ci, va, d, rp.cpu().numpy().astype(np.int64), ns)
+                break
+        else:
+            raise KeyError(name)
+    return _MATS[key]
+
+
+def _suite_names():
+    from paper_2202_08556_b200 import gen
+
+    return [n for n, _ in gen.suite(device="cpu")]
+
+
+@pytest.mark.parametrize("name", _suite_names())
+def test_suite_every_selected_call(env, name):
+    """configs[1] at full size: all seven N of each matrix through DA-SpMM."""
+    torch, gen, sk, model = env
+    M, K, rp, ci, va, d, rp_h, ns = _matrix(env, "suite", name)
+    rows = S.sample_rows(rp_h, seed=len(name))
+    for n in ns:
+        B = gen.dense_operand(K, n, seed=n)
+        C = torch.full((M, n), float("nan"), device="cuda")
+        kout = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+        sk.spmm_selected(d, model, B, C, kernel_out=kout)
+        torch.cuda.synchronize()
+        kid = int(kout.item())
+        f = sk.extract_features(d, n)
+        assert kid == sk.predict_kernel(model, f).index(), (name, n, kid)
+        res = S.check(rp, ci, va, K, B, C, rows)
+        assert res["ok"], (name, n, sk.KernelId.from_index(kid).name(), res)
+
+
+# (workload, matrix, N, kernel, env knobs, expected plan_info variant)
+VARIANTS = [
+    ("suite", "uniform_s20_d16", 2, 4, {}, "eb_thread"),        # one-lane staged (TMA bulk)
+    ("suite", "uniform_s20_d16", 4, 4, {}, "eb_thread"),        # V = 4, 7 pairs per thread
+    ("suite", "uniform_s20_d16", 2, 0, {}, "lean"),             # one-lane RB quad walk
+    ("suite", "uniform_s20_d16", 128, 0, {}, "base"),           # two 64-column y-tiles
+    ("suite", "uniform_s20_d16", 32, 0, {"DASPMM_LEAN_RB": "1"}, "lean"),
+    ("suite", "powerlaw_s20_d16", 16, 4, {}, "lean"),           # range walk, 128 pairs
+    ("suite", "powerlaw_s20_d16", 32, 4, {}, "eb_cta"),         # 256-pair sub-chunks
+    ("suite", "powerlaw_s20_d16", 128, 4, {}, "eb_cta"),        # full-warp groups
+    ("suite", "powerlaw_s20_d16", 64, 4, {"DASPMM_EB_CTA": "0", "DASPMM_EB_CHUNK": "256"},
+     "base"),                                                   # k_eb_sr, 256-pair chunks
+    ("suite", "powerlaw_s20_d16", 64, 4, {"DASPMM_TMA": "1"}, "eb_tma"),
+    ("suite", "powerlaw_s20_d16", 8, 5, {}, "base"),            # EB+PR, conditional scan
+    ("suite", "uniform_s20_d16", 8, 1, {}, "base"),             # RB+PR, tree
+    ("suite", "banded_s20_b8", 128, 0, {"DASPMM_WIN": "1"}, "rb_window"),
+    ("suite", "banded_s20_b8", 2, 4, {}, "eb_thread"),
+    ("suite", "uniform_s17_d16", 8, 2, {}, "base"),             # CM kernels (col-major B)
+    ("suite", "uniform_s17_d16", 8, 3, {}, "base"),
+    ("suite", "powerlaw_s17_d16", 8, 6, {}, "base"),
+    ("suite", "powerlaw_s17_d16", 8, 7, {}, "base"),
+    ("c3", "c3_reddit_like", 128, 4, {}, "lean"),               # segment walk, long rows
+]
+
+
+@pytest.mark.parametrize("case", VARIANTS, ids=[f"{c[1]}-N{c[2]}-k{c[3]}-{c[5]}"
+                                                for c in VARIANTS])
+def test_launch_variants_at_scale(env, case):
+    torch, gen, sk, _ = env
+    workload, name, n, kid, knobs, want = case
+    M, K, rp, ci, va, d, rp_h, _ = _matrix(env, workload, name)
+    old = {k: os.environ.get(k) for k in knobs}
+    os.environ.update(knobs)
+    sk.reload_env()
+    try:
+        B = gen.dense_operand(K, n, seed=100 + n)
+        cm = (kid >> 1) & 1
+        Bop = B.t().contiguous() if cm else B
+        C = torch.full((M, n), float("nan"), device="cuda")
+        if not cm:
+            variant, _ = sk.plan_info(kid, d, B, C)
+            assert variant == want, (case, variant)
+        sk.spmm_device(kid, d, Bop, C)
+        torch.cuda.synchronize()
+        res = S.check(rp, ci, va, K, Bop if cm else B, C, S.sample_rows(rp_h, seed=kid + n),
+                      b_colmajor=bool(cm))
+        assert res["ok"], (case, res)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        sk.reload_env()
+
+
+def test_c1_against_reference_spmm(env):
+    """configs[0] on the reference's own CPU path (oracle/_ref: the unmodified headers):
+    the same R-MAT (rmat.hpp) and dense X (types.hpp:185-193) from the reference's
+    generators; exact mode reproduces its spmm() bits."""
+    torch, gen, sk, _ = env
+    R = O.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built (needs the reference tree at build time)")
+    import ctypes as C
+
+    h = R.ref_rmat(12, 167_772, 0.25, 0.25, 0.25, 0.25, 2022)
+    M, K, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    R.ref_csr_info(h, C.byref(M), C.byref(K), C.byref(nnz))
+    rp = np.zeros(M.value + 1, np.int64)
+    ci = np.zeros(nnz.value, np.int64)
+    va = np.zeros(nnz.value, np.float64)
+    R.ref_csr_copy(h, rp, ci, va)
+    assert nnz.value > 160_000
+    n = 32
+    x = np.zeros(K.value * n, np.float32)
+    R.ref_dense_random_f32(K.value, n, 0, 5, x)  # RowMajor
+    a32 = sk.CsrMatrix(M.value, K.value, rp, ci, va.astype(np.float32), np.float32)
+    d = sk.DeviceCsr.from_host(a32)
+    xl = x.reshape(K.value, n)
+    for kid in range(8):
+        P, W, Cb = 4, 8, 4
+        cm = (kid >> 1) & 1
+        xm = np.ascontiguousarray(xl.T if cm else xl).reshape(-1)
+        want = np.zeros(M.value * n, np.float32)
+        assert R.ref_spmm_f32(h, kid, P, W, Cb, xm, n, int(cm), want) == 0
+        got = sk.spmm(sk.KernelId.from_index(kid), a32,
+                      sk.DenseMatrix.from_logical(xl, sk.Layout.ColMajor if cm else sk.Layout.RowMajor),
+                      sk.WorkerConfig(P, W, Cb), exact=True)
+        g = got.data.reshape(M.value, n)
+        w = want.reshape(M.value, n)
+        if kid < 4:
+            assert np.array_equal(g.view(np.uint32), w.view(np.uint32)), kid
+        else:
+            a = sk.CsrMatrix(M.value, K.value, rp, ci, va, np.float64)
+            import helpers as Hh
+
+            shared = Hh.split_rows(a, P)
+            assert np.array_equal(g[~shared].view(np.uint32), w[~shared].view(np.uint32)), kid
+            assert np.allclose(g[shared], w[shared], rtol=1e-3, atol=1e-6), kid
+    R.ref_csr_free(h)
+    del d
+
+
+@pytest.mark.parametrize("workload,name", [("c3", "c3_reddit_like"),
+                                           ("c4", "c4_rmat_s22_graph500"),
+                                           ("c4", "c4_rmat_s22_a0.7")])
+def test_c3_c4_row_sampled(env, workload, name):
+    torch, gen, sk, model = env
+    M, K, rp, ci, va, d, rp_h, ns = _matrix(env, workload, name)
+    rows = S.sample_rows(rp_h, n_random=256, seed=3)
+    for n in ns:
+        B = gen.dense_operand(K, n, seed=n)
+        C = torch.full((M, n), float("nan"), device="cuda")
+        kout = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+        sk.spmm_selected(d, model, B, C, kernel_out=kout)
+        torch.cuda.synchronize()
+        res = S.check(rp, ci, va, K, B, C, rows)
+        assert res["ok"], (name, n, int(kout.item()), res)
+        del B, C
+        torch.cuda.empty_cache()
+
+
+def test_c5_row_and_column_sampled(env):
+    """configs[4] on one GPU: R-MAT s25, ~503M nnz, N = 256 (B and C 34 GB each)."""
+    torch, gen, sk, model = env
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * (1 << 30):
+        pytest.skip("c5 needs ~80 GB of free device memory")
+    _MATS.clear()
+    torch.cuda.empty_cache()
+    M, K, rp, ci, va, d, rp_h, ns = _matrix(env, "c5", "c5_rmat_s25")
+    n = ns[0]
+    B = gen.dense_operand(K, n, seed=25)
+    C = torch.full((M, n), float("nan"), device="cuda")
+    kout = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    sk.spmm_selected(d, model, B, C, kernel_out=kout)
+    torch.cuda.synchronize()
+    rows = S.sample_rows(rp_h, n_random=192, seed=5, n_boundary=24)
+    cols = np.unique(np.random.default_rng(6).integers(0, n, size=48))
+    res = S.check(rp, ci, va, K, B, C, rows, cols=cols)
+    assert res["ok"], (int(kout.item()), res)
+    del B, C
+    _MATS.clear()
+    torch.cuda.empty_cache()
