@@ -552,9 +552,42 @@ bool tolerance_equal(const DenseMatrix<T>& y, const DenseMatrix<T>& ref,
 }
 
 // ------------------------------------------------------------------ reductions
-/// tree_reduce / conditional_reduce (reduce.hpp:46-102): the reduction networks the
-/// PR kernels implement with warp shuffles, exposed on the host with the reference's
-/// contract (power-of-two widths, nondecreasing segment ids).
+/// The reduction networks the PR kernels implement with warp shuffles
+/// (reduce.hpp:18-102), on the host with the reference's contract.
+namespace detail {
+
+/// Adjacent-pair merge tree over `w` slots of `lanes` values each (slot-major): level
+/// by level slot i becomes slot 2i + slot 2i+1 until slot 0 holds the total. In place:
+/// slot i is written only after slots 2i and 2i+1 (>= i) were read. reduce.hpp:18-25.
+template <class T>
+void tree_reduce_lanes(T* v, std::size_t w, std::size_t lanes) {
+    for (std::size_t width = w; width > 1; width >>= 1) {
+        const std::size_t pairs = width >> 1;
+        for (std::size_t i = 0; i < pairs; ++i) {
+            T* dst = v + i * lanes;
+            const T* a = v + (2 * i) * lanes;
+            const T* b = a + lanes;
+            for (std::size_t c = 0; c < lanes; ++c) dst[c] = a[c] + b[c];
+        }
+    }
+}
+
+/// Gated suffix scan over `w` slots: at distance d = 1, 2, 4, ... slot i adds slot
+/// i + d when both carry the same segment id, so each segment's first slot ends with
+/// the segment total. Ascending i reads slot i + d before it is updated. reduce.hpp:31-39.
+template <class T>
+void conditional_scan_lanes(T* v, const Index* ids, std::size_t w, std::size_t lanes) {
+    for (std::size_t d = 1; d < w; d <<= 1)
+        for (std::size_t i = 0; i + d < w; ++i)
+            if (ids[i] == ids[i + d]) {
+                T* dst = v + i * lanes;
+                const T* src = v + (i + d) * lanes;
+                for (std::size_t c = 0; c < lanes; ++c) dst[c] += src[c];
+            }
+}
+
+}  // namespace detail
+
 template <class T>
 T tree_reduce(std::span<const T> values) {
     const std::size_t w = values.size();
@@ -562,8 +595,7 @@ T tree_reduce(std::span<const T> values) {
         throw std::invalid_argument("tree_reduce: length must be a power of two, got " +
                                     std::to_string(w));
     std::vector<T> v(values.begin(), values.end());
-    for (std::size_t half = w / 2; half >= 1; half /= 2)
-        for (std::size_t i = 0; i < half; ++i) v[i] = v[2 * i] + v[2 * i + 1];
+    detail::tree_reduce_lanes(v.data(), w, 1);
     return v[0];
 }
 
@@ -593,9 +625,7 @@ ConditionalReduceResult<T> conditional_reduce(std::span<const T> values,
             throw std::invalid_argument("conditional_reduce: segment_ids decreasing at index " +
                                         std::to_string(i));
     std::vector<T> v(values.begin(), values.end());
-    for (std::size_t d = 1; d < w; d *= 2)
-        for (std::size_t i = 0; i + d < w; ++i)
-            if (ids[i] == ids[i + d]) v[i] += v[i + d];
+    detail::conditional_scan_lanes(v.data(), ids.data(), w, 1);
     ConditionalReduceResult<T> out;
     for (std::size_t i = 0; i < w; ++i)
         if (i == 0 || ids[i] != ids[i - 1]) out.sums.push_back({ids[i], v[i]});
