@@ -106,6 +106,14 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _key(c):
+    """Call label: matrix/N, plus the column slice for an N-split share."""
+    k = f'{c["m"]["name"]}/N{c.get("n_full", c["n"])}'
+    if c.get("n_full", c["n"]) != c["n"]:
+        k += f'[cols {c["cols"][0]}:{c["cols"][1]}]'
+    return k
+
+
 def _flush(buf):
     """Evicts L2 between timed calls with a READ sweep of a buffer twice the L2 size:
     the lines it leaves are clean, so the next call pays no write-back for them (a
@@ -151,9 +159,11 @@ def build_suite(small: bool, rank: int, world: int, workload: str = "suite"):
 
 def shard_calls(mats, ns_override, rank: int, world: int):
     """This rank's share of the workload's (matrix, N) calls (multi.schedule_units):
-    large calls as nnz-balanced row panels (panel `rank` of each), the rest whole,
-    longest first to the least loaded rank. Returns [(matrix, N, handle, (r0, r1))]
-    and the list of every unit (for the whole-job flop count)."""
+    large calls split across all ranks by daspmm_multi_plan — nnz-balanced row panels
+    with B replicated, or, where it moves fewer bytes per GPU (wide B, e.g. c5 N = 256),
+    N-split column slices with A replicated — the rest whole, longest first to the least
+    loaded rank. Returns [(matrix, N, handle, (r0, r1), (c0, c1))] and every unit (for the
+    whole-job flop count)."""
     import torch
 
     from paper_2202_08556_b200 import multi
@@ -161,23 +171,28 @@ def shard_calls(mats, ns_override, rank: int, world: int):
     units = [(m, n) for m in mats for n in (ns_override or m["ns"])]
     costs = [multi.estimate_call_us(m["nnz_total"], n) for m, n in units]
     # DASPMM_SPLIT_FRAC (default 0.5) forces more row splitting, e.g. to exercise the
-    # panel path and C assembly on 2 ranks.
+    # panel path and C assembly on 2 ranks; DASPMM_SPLIT_MODE=rows|cols forces the split.
     assign, split = multi.schedule_units(costs, world,
                                          float(os.environ.get("DASPMM_SPLIT_FRAC", "0.5")))
+    force = {"rows": multi.SPLIT_ROWS, "cols": multi.SPLIT_COLS}.get(
+        os.environ.get("DASPMM_SPLIT_MODE", ""), multi.SPLIT_AUTO)
     panels = {}
     mine = []
     for i in assign[rank]:
         m, n = units[i]
         if split[i]:
+            mode, bounds = multi.plan(m["full"], world, n, force)
+            lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+            if mode == "cols":
+                mine.append((m, n, m["full"], (0, m["M"]), (lo, hi)))
+                continue
             if m["name"] not in panels:
-                cuts = multi.row_panel_cuts(m["rp"].cpu().numpy(), world)
-                r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-                panels[m["name"]] = (m["full"].panel(r0, r1), (r0, r1))
+                panels[m["name"]] = (m["full"].panel(lo, hi), (lo, hi))
                 torch.cuda.synchronize()
             d, rows = panels[m["name"]]
         else:
             d, rows = m["full"], (0, m["M"])
-        mine.append((m, n, d, rows))
+        mine.append((m, n, d, rows, (0, n)))
     return mine, units
 
 
@@ -211,13 +226,16 @@ def run_ours(args):
     # Operands per (matrix, N) call of this rank: B replicated, C the local panel.
     mine, units = shard_calls(mats, ns_override, rank, world)
     calls = []
-    for m, n, d, rows in mine:
+    for m, n, d, rows, (c0, c1) in mine:
         B = gen.dense_operand(m["K"], n, seed=1000 + n, device=dev)
-        Cp = torch.empty(d.num_rows, n, device=dev)
+        w = c1 - c0
+        if w != n:  # N-split: this rank's column slice of the replicated-seed B
+            B = B[:, c0:c1].contiguous()
+        Cp = torch.empty(d.num_rows, w, device=dev)
         kout = torch.zeros(1, dtype=torch.int32, device=dev)
-        calls.append(dict(m=m, n=n, d=d, rows=rows, B=B, C=Cp, kout=kout,
-                          flops=gen.flops(d.nnz(), n),
-                          bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), n, d.cols_touched)))
+        calls.append(dict(m=m, n=w, n_full=n, cols=(c0, c1), d=d, rows=rows, B=B, C=Cp,
+                          kout=kout, flops=gen.flops(d.nnz(), w),
+                          bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), w, d.cols_touched)))
     stream = torch.cuda.current_stream(dev)
 
     def one(c):
@@ -275,7 +293,7 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
-        key = f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}'
+        key = _key(calls[dom])
         traffic = tr.get(key)
     except Exception:
         pass
@@ -325,7 +343,7 @@ def _warm(calls, one, stream, world, dev, total_flops, reps=3):
     dom = max(range(len(calls)), key=lambda i: per[i])
     return {"value": round(total_flops / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
             "ms_per_step": round(ms, 4),
-            "dominant": {"call": f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}',
+            "dominant": {"call": _key(calls[dom]),
                          "ms": round(per[dom], 4)},
             "protocol": f"no L2 flush; each call {reps}x back to back, mean of the last {reps - 1}"}
 
@@ -390,7 +408,7 @@ def _parity_map(calls):
         rp_h = rp_h - rp_h[0]
         rows = S.sample_rows(rp_h, n_random=128, n_boundary=8, seed=c["n"])
         res = S.check(m["rp"], m["ci"], m["va"], m["K"], c["B"], c["C"], rows + r0, row0=r0)
-        key = f'{m["name"]}/N{c["n"]}'
+        key = _key(c)
         out[key] = round(res["max_ratio"], 4)
         worst = max(worst, res["max_ratio"])
         if not res["ok"]:
@@ -410,37 +428,44 @@ def _assembly(calls, mats, world, dev):
 
     from paper_2202_08556_b200 import multi
 
-    split = [c for c in calls if c["rows"] != (0, c["m"]["M"])]
-    big = max(split, key=lambda c: c["m"]["M"] * c["n"]) if split else None
-    name = f'{big["m"]["name"]}/N{big["n"]}' if big else None
+    split = [c for c in calls if c["rows"] != (0, c["m"]["M"]) or c["n"] != c["n_full"]]
+    big = max(split, key=lambda c: c["m"]["M"] * c["n_full"]) if split else None
+    name = _key(big) if big else None
     names = [None] * world
     import torch.distributed as dist
 
     dist.all_gather_object(names, name)
     if len(set(names)) != 1 or name is None:  # every rank must join the same collective
         return None
-    full_bytes = big["m"]["M"] * big["n"] * 4
+    full_bytes = big["m"]["M"] * big["n_full"] * 4
     if full_bytes > (8 << 30):  # c5: 34 GB per GPU, more than the SpMM itself moves
         return {"call": name, "ms": None, "bytes_per_rank": full_bytes,
                 "skipped": "assembled C above 8 GB per GPU"}
-    cuts = multi.row_panel_cuts(big["m"]["rp"].cpu().numpy(), world)
-    full = multi.gather_rows(big["C"], cuts)  # warm-up (communicator set-up)
+    by_cols = big["n"] != big["n_full"]
+    if by_cols:
+        bounds = multi.col_split(big["n_full"], world)
+        gather = lambda: multi.gather_cols(big["C"], bounds)  # noqa: E731
+    else:
+        _, cuts = multi.plan(big["m"]["full"], world, big["n_full"], multi.SPLIT_ROWS)
+        gather = lambda: multi.gather_rows(big["C"], cuts)  # noqa: E731
+    full = gather()  # warm-up (communicator set-up)
     torch.cuda.synchronize()
     dist.barrier()
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     s.record()
-    full = multi.gather_rows(big["C"], cuts)
+    full = gather()
     e.record()
     torch.cuda.synchronize()
     ms = _max_over_ranks(s.elapsed_time(e), dev)
     nbytes = full.numel() * full.element_size()
     out = {"call": name, "ms": round(ms, 4), "bytes_per_rank": nbytes,
-           "collective": "all-gather of padded row panels (multi.gather_rows)"}
+           "collective": "all-gather of padded column slices (multi.gather_cols)" if by_cols
+           else "all-gather of padded row panels (multi.gather_rows)"}
     # Fused alternative (NCCL runs only, one rank per GPU): the RB+RM+SR panel kernel
     # stores every finished row into all ranks' copies of C (symmetric memory over
     # NVLink); its time includes the SpMM itself.
-    if dist.get_backend() == "nccl":
+    if dist.get_backend() == "nccl" and not by_cols:
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
@@ -546,7 +571,7 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                      "peak_source": peak_kind,
                      "scope": "dominant call (longest of the step): its algorithmic bytes "
                               "(4(M+1)+8nnz+4N*K_touched+4NM) / its mean CUDA-event time",
-                     "dominant": {"call": f'{calls[dom]["m"]["name"]}/N{calls[dom]["n"]}',
+                     "dominant": {"call": _key(calls[dom]),
                                   "kernel": sk.KernelId.from_index(chosen[dom]).name(),
                                   "ms": round(per_call_ms[dom], 4),
                                   "algorithmic_bytes": calls[dom]["bytes"],
@@ -555,9 +580,9 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                                          "frac": round(achieved / peak, 4),
                                          "scope": "sum algorithmic bytes / sum call time"}},
         "clocks": clk.summary(),
-        "selected": {f'{c["m"]["name"]}/N{c["n"]}': sk.KernelId.from_index(k).name()
+        "selected": {_key(c): sk.KernelId.from_index(k).name()
                      for c, k in zip(calls, chosen)},
-        "per_call_ms": {f'{c["m"]["name"]}/N{c["n"]}': round(t, 5)
+        "per_call_ms": {_key(c): round(t, 5)
                         for c, t in zip(calls, per_call_ms)},
         "parity": parity,
         "warm_l2": warm,
@@ -714,9 +739,9 @@ def _cusparse_compare(calls, flush, our_ms, ns, reps=5):
             "algorithms": [f"{o}:{a}" for o in ("row", "col") for a in CUSPARSE_ALGS],
             "statistic": f"mean of {reps} runs, L2 flushed before each (same as ours)",
             "ms_per_step": round(cus_ms, 4),
-            "per_call_ms": {f'{c["m"]["name"]}/N{c["n"]}': round(b, 5)
+            "per_call_ms": {_key(c): round(b, 5)
                             for c, b in zip(calls, best)},
-            "winner_per_call": {f'{c["m"]["name"]}/N{c["n"]}': w for c, w in zip(calls, winner)},
+            "winner_per_call": {_key(c): w for c, w in zip(calls, winner)},
             "winner_counts": wins,
             "speedup_geomean": round(geo, 4) if geo else None,
             "speedup_geomean_by_N": {str(n): round(statistics.geometric_mean(v), 4)

@@ -186,6 +186,33 @@ int daspmm_spmm_selected(const daspmm_csr* csr, const daspmm_model* model, int64
                          int64_t ldc, int64_t W, unsigned flags, int* d_kernel,
                          daspmm_stream stream);
 
+/* ---------------------------------------------------------------- multi-GPU (§8e)
+ * One process per GPU. A communicator wraps NCCL (loaded at run time from
+ * libnccl.so.2; DASPMM_ERR_NCCL when absent): rank 0 makes the 128-byte unique id, the
+ * caller distributes it (e.g. torch.distributed broadcast), every rank creates its
+ * communicator on its current device. */
+typedef struct daspmm_comm daspmm_comm;
+enum { DASPMM_SPLIT_AUTO = -1, DASPMM_SPLIT_ROWS = 0, DASPMM_SPLIT_COLS = 1 };
+int daspmm_comm_unique_id(void* id_out /* 128 bytes */);
+int daspmm_comm_create(int nranks, int rank, const void* unique_id, daspmm_comm** out);
+int daspmm_comm_destroy(daspmm_comm* comm);
+/* Partition of C = A·B over `parts` GPUs. mode DASPMM_SPLIT_ROWS: nnz-balanced row
+ * panels, bounds[p] = row holding partition_elements' chunk p start (partition.hpp:
+ * 45-64, snapped to row starts, nondecreasing), B replicated; DASPMM_SPLIT_COLS: column
+ * slices bounds[p] = floor(N p / parts), A replicated; DASPMM_SPLIT_AUTO: the one with
+ * fewer per-GPU compulsory bytes (rows: A/P + B + C/P, cols: A + B/P + C/P). bounds has
+ * parts + 1 entries (host). */
+int daspmm_multi_plan(const daspmm_csr* csr, int parts, int64_t N, int mode, int* mode_out,
+                      int64_t* bounds);
+/* The calling rank's exchange-free share of C = A·B by DA-SpMM (device selector on the
+ * share), written into its rows / columns of the full M x N row-major d_C; with
+ * assemble != 0 the other ranks' shares are then gathered over NCCL (rows: one broadcast
+ * per panel in one group, needs ldc == N; cols: pack, all-gather, unpack). `csr` is the
+ * full matrix on this rank's device (row panels are built once and cached on it); comm
+ * NULL = one rank. Asynchronous on `stream`. */
+int daspmm_multi_spmm(daspmm_comm* comm, const daspmm_csr* csr, const daspmm_model* model,
+                      int64_t hw, const void* d_B, int64_t ldb, int64_t N, void* d_C, int64_t ldc,
+                      int mode, int assemble, int* d_kernel, daspmm_stream stream);
 /* Graph-cache occupancy of a handle: instantiated graphs, retired graphs awaiting
  * completion, and known (model, N, hw) decisions. Diagnostics for tests. */
 int daspmm_selected_cache_info(const daspmm_csr* csr, int64_t* graphs, int64_t* retired,

@@ -24,6 +24,7 @@ F32, F64 = 0, 1
 ROW_MAJOR, COL_MAJOR = 0, 1
 EXACT = 1
 RESELECT = 2
+SPLIT_AUTO, SPLIT_ROWS, SPLIT_COLS = -1, 0, 1
 
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -63,6 +64,12 @@ SIGNATURES = {
     "daspmm_plan_info": (C.c_int, [_vp, C.c_int, _i64, _vp, _i64, _vp, _i64, C.c_uint, _vp, _vp]),
     "daspmm_debug_conditional_scan_f64": (C.c_int, [_vp, _vp, _i64, _vp]),
     "daspmm_selected_cache_info": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
+    "daspmm_comm_unique_id": (C.c_int, [_vp]),
+    "daspmm_comm_create": (C.c_int, [C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
+    "daspmm_comm_destroy": (C.c_int, [_vp]),
+    "daspmm_multi_plan": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _ip, _vp]),
+    "daspmm_multi_spmm": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, C.c_int,
+                                    C.c_int, _vp, _vp]),
 }
 
 _lib = None

@@ -30,7 +30,8 @@ CFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcom
                  "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 
 LIB_SOURCES = ["abi.cu", "features.cu", "select.cu", "graph.cu", "spmm_rb_sr.cu",
-               "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu", "spmm_tma.cu"]
+               "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu", "spmm_tma.cu",
+               "multi.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "dispatch.h", "internal.h", "launch_sr.cuh",
            "launch_pr.cuh", "lean.cuh", "tma_gather.cuh"]
 
@@ -62,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), LIB_SOURCES))
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

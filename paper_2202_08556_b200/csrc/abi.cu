@@ -818,6 +818,8 @@ int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1, dasp
 int daspmm_csr_destroy(daspmm_csr* h) {
     if (!h) return DASPMM_OK;
     graph_cache_free(h);
+    for (auto& e : h->panels) daspmm_csr_destroy(e.h);
+    h->panels.clear();
     if (h->owns) {
         cudaFree(h->rp);
         cudaFree(h->ci);

@@ -67,6 +67,13 @@ struct daspmm_csr {
     static constexpr int kSpanLevels = 8;
     int64_t span_max[kSpanLevels] = {};
     double span_avg[kSpanLevels] = {};
+    // Row-panel handles built by daspmm_multi_spmm (one per (parts, rank)), destroyed
+    // with this handle (multi.cu).
+    struct PanelEntry {
+        int parts, rank;
+        daspmm_csr* h;
+    };
+    std::vector<PanelEntry> panels;
 };
 
 namespace daspmm {

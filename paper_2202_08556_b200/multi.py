@@ -90,6 +90,79 @@ def col_split(N: int, parts: int):
     return [(N * p) // parts for p in range(parts + 1)]
 
 
+SPLIT_AUTO, SPLIT_ROWS, SPLIT_COLS = -1, 0, 1
+
+
+def plan(d, parts: int, N: int, mode: int = SPLIT_AUTO):
+    """daspmm_multi_plan on a DeviceCsr: ('rows' | 'cols', bounds[parts + 1]). Rows: nnz-
+    balanced cuts at partition_elements' chunk starts (device partition kernel); cols:
+    floor(N p / parts); auto: fewer per-GPU compulsory bytes."""
+    import ctypes as C
+
+    from . import _lib
+
+    out_mode = C.c_int()
+    bounds = np.zeros(parts + 1, dtype=np.int64)
+    _lib.check(_lib.lib().daspmm_multi_plan(d._h, parts, N, mode, C.byref(out_mode),
+                                            bounds.ctypes.data))
+    return ("rows" if out_mode.value == SPLIT_ROWS else "cols"), bounds
+
+
+class Comm:
+    """NCCL communicator of the C ABI (daspmm_comm) for one rank of a torch.distributed
+    job: rank 0 makes the unique id, the process group broadcasts it."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        uid = bytearray(128)
+        if self.rank == 0:
+            buf = (C.c_char * 128)()
+            _lib.check(_lib.lib().daspmm_comm_unique_id(buf))
+            uid = bytearray(buf.raw)
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        raw = (C.c_char * 128).from_buffer_copy(box[0])
+        self._c = C.c_void_p()
+        _lib.check(_lib.lib().daspmm_comm_create(self.nranks, self.rank, raw, C.byref(self._c)))
+
+    def close(self):
+        from . import _lib
+
+        if self._c:
+            _lib.lib().daspmm_comm_destroy(self._c)
+            self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def spmm(comm, d, model, B, C_full, mode: int = SPLIT_AUTO, assemble: bool = False,
+         kernel_out=None, hw: int = -1, stream=None):
+    """daspmm_multi_spmm: this rank's exchange-free share of C = A·B by DA-SpMM into its
+    rows / columns of C_full (M x N row-major on every rank); with ``assemble`` the
+    shares of all ranks are gathered over NCCL. ``comm`` None = a single rank."""
+    from . import _lib
+    from . import spmmkit as sk
+
+    sk._check_operands(d, B, C_full, sk.Layout.RowMajor, "multi_spmm")
+    kp = kernel_out.data_ptr() if kernel_out is not None else None
+    _lib.check(_lib.lib().daspmm_multi_spmm(comm._c if comm is not None else None, d._h, model._m,
+                                            hw, B.data_ptr(), sk._ld(B), B.shape[1],
+                                            C_full.data_ptr(), sk._ld(C_full), mode,
+                                            1 if assemble else 0, kp, sk._stream_ptr(stream)))
+    return C_full
+
+
 def choose_partition(M: int, K: int, nnz: int, N: int, parts: int, elem: int = 4) -> str:
     """Pick 'rows' or 'cols' by per-GPU compulsory bytes:
     rows: A/P + B + C/P ; cols: A + B/P + C/P."""
@@ -112,11 +185,12 @@ def gather_rows(local_c, cuts, group=None):
     sizes = [int(cuts[p + 1] - cuts[p]) for p in range(world)]
     mx = max(sizes)
     n = local_c.shape[1]
-    pad = torch.zeros(mx, n, dtype=local_c.dtype, device=local_c.device)
+    dev = _comm_device(local_c, group)
+    pad = torch.zeros(mx, n, dtype=local_c.dtype, device=dev)
     pad[: local_c.shape[0]].copy_(local_c)
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
-    return torch.cat([outs[p][: sizes[p]] for p in range(world)], 0)
+    return torch.cat([outs[p][: sizes[p]] for p in range(world)], 0).to(local_c.device)
 
 
 def gather_cols(local_c, bounds, group=None):
@@ -125,14 +199,23 @@ def gather_cols(local_c, bounds, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    widths = [bounds[p + 1] - bounds[p] for p in range(world)]
+    widths = [int(bounds[p + 1] - bounds[p]) for p in range(world)]
     mx = max(widths)
     M = local_c.shape[0]
-    pad = torch.zeros(M, mx, dtype=local_c.dtype, device=local_c.device)
+    dev = _comm_device(local_c, group)
+    pad = torch.zeros(M, mx, dtype=local_c.dtype, device=dev)
     pad[:, : local_c.shape[1]].copy_(local_c)
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
-    return torch.cat([outs[p][:, : widths[p]] for p in range(world)], 1)
+    return torch.cat([outs[p][:, : widths[p]] for p in range(world)], 1).to(local_c.device)
+
+
+def _comm_device(t, group=None):
+    """Where the collective's buffers live: the tensor's device under NCCL, host memory
+    under gloo (the multi-rank logic is exercised with gloo on CPU-only or 1-GPU hosts)."""
+    import torch.distributed as dist
+
+    return "cpu" if dist.get_backend(group) == "gloo" else t.device
 
 
 def spmm_rows_allgather(panel, B, M: int, r0: int, group=None, C_full=None):
