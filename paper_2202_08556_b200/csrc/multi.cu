@@ -231,7 +231,7 @@ int daspmm_multi_spmm(daspmm_comm* comm, const daspmm_csr* h, const daspmm_model
                                           d_kernel, stream))
             return rc;
     }
-    if (!assemble || parts == 1) return DASPMM_OK;
+    if (!assemble || comm == nullptr) return DASPMM_OK;  // one rank with a comm: the NCCL path still runs
     // ---- assembly over NCCL
     const ncclDataType_t dt = h->dtype == DASPMM_F64 ? ncclDouble : ncclFloat;
     ncclResult_t nr;
