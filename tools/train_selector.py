@@ -55,6 +55,42 @@ def normalized(times, chosen):
     return times.min(1) / times[np.arange(len(times)), chosen]
 
 
+def cross_validate(R, ids, feats, times, k, train, predict, seed=2202):
+    """K folds by matrix. Fold f is scored by a model trained on the other folds (7/8 of
+    their matrices for training, 1/8 for the trainer's validation / early stopping)."""
+    mats = sorted(set(ids))
+    rng = np.random.default_rng(seed)
+    rng.shuffle(mats)
+    fold_of = {m: i % k for i, m in enumerate(mats)}
+    fold = np.array([fold_of[i] for i in ids])
+    chosen = np.zeros(len(ids), dtype=np.int64)
+    per_fold = []
+    for f in range(k):
+        rest = [m for m in mats if fold_of[m] != f]
+        n_va = max(1, len(rest) // 8)
+        va_set = set(rest[:n_va])
+        tr = np.array([i for i in range(len(ids)) if fold[i] != f and ids[i] not in va_set])
+        va = np.array([i for i in range(len(ids)) if fold[i] != f and ids[i] in va_set])
+        text = train(np.concatenate([tr, va]), len(tr))
+        m = R.ref_selector_load(text.encode())
+        te = np.where(fold == f)[0]
+        for i in te:
+            chosen[i] = predict(m, i)
+        R.ref_selector_free(m)
+        s = normalized(times[te], chosen[te])
+        per_fold.append(round(float(np.exp(np.log(s).mean())), 4))
+    sel = normalized(times, chosen)
+    static = {NAMES[j]: float(np.exp(np.log(normalized(times, np.full(len(ids), j))).mean()))
+              for j in range(8)}
+    best = max(static, key=static.get)
+    return {"folds": k, "by": "matrix", "samples": len(ids), "matrices": len(mats),
+            "selector_geomean_normalized": round(float(np.exp(np.log(sel).mean())), 4),
+            "selector_accuracy": round(float((chosen == times.argmin(1)).mean()), 4),
+            "per_fold_geomean": per_fold,
+            "best_static": best, "best_static_geomean": round(static[best], 4),
+            "note": "every sample scored by a model trained without its matrix"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
@@ -65,6 +101,9 @@ def main():
     ap.add_argument("--min-leaf", type=int, default=5)
     ap.add_argument("--final", action="store_true",
                     help="after evaluating, retrain on train+valid+test (deployment model)")
+    ap.add_argument("--cv", type=int, default=0,
+                    help="also K-fold cross-validate by matrix: every matrix is scored by a model "
+                         "that never saw it (the held-out score of the deployed procedure)")
     a = ap.parse_args()
     R = O.ref()
     assert R is not None, "needs oracle/_ref (reference trainer); run make -C oracle"
@@ -106,6 +145,8 @@ def main():
     report["best_static"] = max(static, key=static.get)
     report["label_histogram_all"] = {NAMES[k]: int((times.argmin(1) == k).sum()) for k in range(8)}
     R.ref_selector_free(model)
+    if a.cv > 1:
+        report["cross_validation"] = cross_validate(R, ids, feats, times, a.cv, train, predict)
     if a.final:
         allidx = np.arange(len(ids))
         text = train(allidx, len(allidx))
