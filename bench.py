@@ -306,6 +306,7 @@ def run_ours(args):
     parity = _parity_map(calls) if rank == 0 else None
     warm = _warm(calls, one, stream, world, dev, total_flops)
     overhead = _da_overhead(calls, model, stream, flush) if rank == 0 else None
+    batched = _batched_small(calls, model, flush, per_call_ms) if rank == 0 else None
     assembly = None
     if world > 1:
         try:
@@ -316,7 +317,42 @@ def run_ours(args):
         _write_roofline_table(args.roofline_table, calls, per_call_ms, chosen, peak)
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-                   flush, assembly, warm, overhead)
+                   flush, assembly, warm, overhead, batched)
+
+
+def _batched_small(calls, model, flush, per_call_ms, reps=5, max_nnz=300_000):
+    """The small calls of the workload (<= 300K nnz: the 2^14-row matrices) as one CUDA
+    graph (spmmkit.SpmmBatch: the chosen kernels' launches, EB prologues included),
+    timed cold (L2 flushed before each replay) against the same calls launched one by
+    one (their per-call times of the main measurement)."""
+    import torch
+
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    idx = [i for i, c in enumerate(calls) if c["d"].nnz() <= max_nnz]
+    if not idx:
+        return None
+    batch = sk.SpmmBatch([(calls[i]["d"], calls[i]["B"], calls[i]["C"]) for i in idx], model)
+    batch.run()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        _flush(flush)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        batch.run()
+        e.record()
+        torch.cuda.synchronize()
+        tot += s.elapsed_time(e)
+    ms = tot / reps
+    one_by_one = sum(per_call_ms[i] for i in idx)
+    return {"calls": len(idx), "graph_ms": round(ms, 4),
+            "us_per_call": round(ms * 1e3 / len(idx), 2),
+            "one_by_one_ms": round(one_by_one, 4),
+            "one_by_one_us_per_call": round(one_by_one * 1e3 / len(idx), 2),
+            "protocol": "spmmkit.SpmmBatch (one graph launch for all of them), L2 flushed once "
+                        f"before each replay, mean of {reps}"}
 
 
 def _warm(calls, one, stream, world, dev, total_flops, reps=3):
@@ -541,7 +577,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
 
 def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
             per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-            flush, assembly=None, warm=None, overhead=None):
+            flush, assembly=None, warm=None, overhead=None, batched=None):
     import torch.distributed as dist
 
     from paper_2202_08556_b200 import spmmkit as sk
@@ -587,6 +623,7 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
         "parity": parity,
         "warm_l2": warm,
         "da_spmm_overhead": overhead,
+        "small_calls_batched": batched,
     }
     if assembly is not None:
         result["assembly"] = assembly
@@ -799,7 +836,7 @@ def _cpu_time_reference(sample, steps):
         h = handles[m["name"]]
         x = np.random.default_rng(n).uniform(-1, 1, (m["K"], n)).astype(np.float32).reshape(-1)
         med, mn, ck = C.c_double(), C.c_double(), C.c_double()
-        rc = R.ref_time_spmm_f32(h, 0, cores, 8, 8, x, n, 3, 1, C.byref(med), C.byref(mn),
+        rc = R.ref_time_spmm_f32(h, 0, cores, 8, 8, x, n, 7, 2, C.byref(med), C.byref(mn),
                                  C.byref(ck))
         if rc:
             raise RuntimeError(R.ref_last_error().decode())
@@ -819,7 +856,7 @@ def _cpu_baseline(mats, ns_override=None, steps=1):
     v, cores, secs = r
     return {"value": round(v, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
             "sample": f"reference spmm() RB+RM+SR fp32, P={cores} threads, time_kernel_fn "
-                      f"(warmup 1, reps 3, median) over all {len(sample)} (matrix, N) pairs of the "
+                      f"(warmup 2, reps 7, median; bench.hpp:63-121) over all {len(sample)} (matrix, N) pairs of the "
                       f"workload (matrices > {REF_PANEL_NNZ} nnz as a middle row panel of that "
                       f"size); {secs:.2f} s of timed CPU work per pass"}
 

@@ -135,6 +135,7 @@ struct Knobs {
     bool tma = false;         // DASPMM_TMA=1: TMA gather4 EB kernel
     int64_t tma_lw = 0;       // DASPMM_TMA_LW: its pairs per warp
     bool fault = false;       // SPMMKIT_ENABLE_FAULT_INJECTION=1 + DASPMM_INJECT_FAULT=1
+    bool pdl = true;          // DASPMM_PDL=0: EB kernels wait for their prologue to finish
     // DASPMM_CTA_THREADS (64/128/256): CTA size of the CTA-combined EB walk. Measured:
     // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
     // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
@@ -171,6 +172,7 @@ static Knobs read_knobs() {
     k.tma = on("DASPMM_TMA", '1');
     k.tma_lw = i64("DASPMM_TMA_LW");
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
+    k.pdl = !on("DASPMM_PDL", '0');
     if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 32 || t == 64 || t == 128 || t == 256) {
         k.cta_threads = int(t);
         k.cta_threads_set = true;
@@ -502,7 +504,14 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     // built before capture).
     if (own_scratch && (kernel >= 4 || !(kernel & 1)))
         if (int rc = ensure_coo(h, s)) return rc;
-    const Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
+    Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
+    if (kernel >= 4 && knobs().pdl) {
+        // Programmatic launch after the EB prologue; not inside a stream capture (graph
+        // bodies keep plain stream order).
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        p.pdl = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+        cudaGetLastError();
+    }
     int* chunk_row = chunk_scratch;
     cudaError_t e;
     if (kernel >= 4 && own_scratch) {

@@ -157,6 +157,18 @@ __device__ __forceinline__ T ld_stream(const T* p) {
     return __ldcs(p);
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The EB prologue (k_eb_prep*) zeroes the rows the EB kernel later deposits into with
+// atomics. The EB kernel is launched with programmatic stream serialization, so its CTAs
+// start (and load A and gather B) while the prologue still runs; it waits for the
+// prologue only before its first atomic deposit (and once more before exiting, so the
+// call as a whole still completes after the prologue). Without the launch attribute the
+// wait returns immediately.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ arithmetic
 template <bool EXACT>
 __device__ __forceinline__ float madd(float acc, float a, float b) {

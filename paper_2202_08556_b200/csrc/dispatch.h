@@ -33,7 +33,42 @@ struct Plan {
     int win_rows = 0;    // RB+SR window kernel (k_rb_sr_win): rows per CTA panel, 0 = off
     bool repl = false;   // RB+SR with the replicated row epilogue (daspmm_spmm_rows_to)
     size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
+    bool pdl = false;    // EB: launch the kernel programmatically after its prologue
 };
+
+// Kernel launch; with pdl, programmatic stream serialization: the kernel may start while
+// the previous kernel of the stream (the EB prologue) still runs — the EB kernels wait
+// for it (griddep_wait, common.cuh) only before their atomic deposits.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args... args) {
+    if (!pdl) {
+        k<<<grid, block, smem, s>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// Launch site of the instantiation tables (`p`, `a`, `s` in scope). A translation unit
+// whose kernels follow a prologue defines DASPMM_PDL_EXPR before including this header.
+#ifndef DASPMM_PDL_EXPR
+#define DASPMM_PDL_EXPR false
+#endif
+#define DASPMM_GO(K, G, NT)                                                          \
+    do {                                                                             \
+        const cudaError_t e_ = launch_k(DASPMM_PDL_EXPR, K, G, dim3(NT), 0, s, a);   \
+        if (e_ != cudaSuccess) return e_;                                            \
+    } while (0)
 
 // Pairs per thread of the one-lane EB+SR path (k_eb_sr_thr). Measured on B200 (uniform
 // s20): V <= 2 takes 12 (4 x odd: 128-bit conflict-free shared reads; N = 2 129 -> 105

@@ -167,8 +167,12 @@ __device__ __forceinline__ void sr_walk(const SpmmArgs<T>& a, const int e0, cons
             }
             if (col < a.N) {
                 const int64_t off = int64_t(r) * a.ldc + col;
-                if (owned) st_frag(a.C + off, out);
-                else atomic_add_frag(a.C + off, out);
+                if (owned) {
+                    st_frag(a.C + off, out);
+                } else {
+                    griddep_wait();  // split row: zeroed by the EB prologue
+                    atomic_add_frag(a.C + off, out);
+                }
                 if constexpr (MODE == kRBRepl) {  // replicated epilogue (daspmm_spmm_rows_to)
                     for (int d = 0; d < a.n_extra; ++d) st_frag(a.extra[d] + off, out);
                 }
@@ -416,13 +420,16 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 8 || LPR <= 2) ? 3 : 4
     const unsigned mask = group_mask<LPR>();
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / LPR;
-    if (w >= a.P) return;
-    int64_t e0, e1;
-    chunk_bounds(a.nnz, a.P, w, e0, e1);
-    if (e0 >= e1) return;
+    int64_t e0 = 0, e1 = 0;
+    if (w < a.P) chunk_bounds(a.nnz, a.P, w, e0, e1);
+    if (e0 >= e1) {
+        griddep_wait();
+        return;
+    }
     const int n0 = blockIdx.y * TN + gl * V;
     sr_walk<T, CM, EXACT, V, LPR, CPL, kEB>(a, int(e0), int(e1), __ldg(a.rows + e0), 0, n0, mask,
                                             gl);
+    griddep_wait();
 }
 
 // EB + SR, fast path: a CTA owns G = 256/LPR consecutive sub-chunks of a.sub pairs,
@@ -466,8 +473,12 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
         T acc = T(0);
         auto deposit = [&](int row, T v) {
             T* y = a.C + int64_t(row) * a.ldc + col;
-            if (__ldg(a.rp + row) >= E0 && __ldg(a.rp + row + 1) <= E1) *y = v;
-            else atomicAdd(y, v);
+            if (__ldg(a.rp + row) >= E0 && __ldg(a.rp + row + 1) <= E1) {
+                *y = v;
+            } else {
+                griddep_wait();
+                atomicAdd(y, v);
+            }
         };
         for (int b = 0; b <= G; ++b) {
             const int row = srow[b];
@@ -483,6 +494,7 @@ k_eb_sr_cta(const SpmmArgs<T> a) {
         }
         if (cur >= 0) deposit(cur, acc);
     }
+    griddep_wait();  // complete only after the prologue (programmatic launch)
 }
 
 // EB + SR, fast path for one-lane groups (N <= V, i.e. N <= 4 in fp32): every thread
@@ -637,10 +649,15 @@ __global__ void __launch_bounds__(NT, 3 * (kThreads / NT)) k_eb_sr_thr(const Spm
     if (seg_start) {
         T* y = a.C + int64_t(first_row) * a.ldc + col0;
         const bool crosses = lane == 0 || (l31_key == key && l31_cont);
-        if (crosses) atomic_add_frag(y, head);
-        else st_frag(y, head);
+        if (crosses) {
+            griddep_wait();
+            atomic_add_frag(y, head);
+        } else {
+            st_frag(y, head);
+        }
     }
     const bool tail_out = has_tail && (lane == 31 || !next_takes);
+    griddep_wait();  // before the tail deposit, and so the grid ends after the prologue
     if (tail_out) atomic_add_frag(a.C + int64_t(last_row) * a.ldc + col0, tail);
 }
 
@@ -653,6 +670,7 @@ __global__ void __launch_bounds__(kThreads)
 k_eb_prep_uniform(const int* __restrict__ rows, int64_t nnz, int64_t stride, int64_t n_bound,
                   T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty,
                   int shift) {
+    griddep_launch_dependents();  // the EB kernel may launch now; it waits before atomics
     const int nvec = (N + VZ - 1) / VZ;
     const int64_t idx = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     // shift >= 0: nvec is a power of two and idx fits 32 bits (host-checked): no 64-bit
@@ -747,6 +765,7 @@ __global__ void __launch_bounds__(kThreads)
 k_eb_prep(const int* __restrict__ rp, int M, int64_t nnz, int64_t P, int* __restrict__ chunk_row,
           T* C, int64_t ldc, int N, const int* __restrict__ empty_rows, int n_empty,
           const int* __restrict__ rows) {
+    griddep_launch_dependents();
     const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (tid < P) {
         int64_t b, e;
@@ -784,10 +803,12 @@ __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
     const unsigned mask = group_mask<W>();
     const int gl = threadIdx.x & (W - 1);
     const int64_t w = (int64_t(blockIdx.x) * kThreads + threadIdx.x) / W;
-    if (w >= a.P) return;
-    int64_t e0l, e1l;
-    chunk_bounds(a.nnz, a.P, w, e0l, e1l);
-    if (e0l >= e1l) return;
+    int64_t e0l = 0, e1l = 0;
+    if (w < a.P) chunk_bounds(a.nnz, a.P, w, e0l, e1l);
+    if (e0l >= e1l) {
+        griddep_wait();
+        return;
+    }
     const int e0 = int(e0l), e1 = int(e1l);
     const int nbase = blockIdx.y * NSLOT * V;
     // Split rows: the chunk's first row if it began before e0, its last row if it
@@ -830,6 +851,7 @@ __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
                     if (seg_start) {
                         T* y = a.C + int64_t(row) * a.ldc + col;
                         if (!owned) {
+                            griddep_wait();
                             atomic_add_frag(y, p);
                         } else if (first) {
                             if constexpr (EXACT) {
@@ -851,6 +873,7 @@ __global__ void __launch_bounds__(kThreads) k_eb_pr(const SpmmArgs<T> a) {
         const int last = min(W, e1 - tb) - 1;
         prev_last = __shfl_sync(mask, row, last, W);
     }
+    griddep_wait();
 }
 
 }  // namespace daspmm

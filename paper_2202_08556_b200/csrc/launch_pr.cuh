@@ -7,8 +7,8 @@
 namespace daspmm {
 
 #define DASPMM_PR_OWN(KERN, T, CM, EXACT, V, W)                                         \
-    if (p.X == 2) KERN<T, CM, EXACT, V, W, 2><<<p.grid, kThreads, 0, s>>>(a);           \
-    else KERN<T, CM, EXACT, V, W, 1><<<p.grid, kThreads, 0, s>>>(a);
+    if (p.X == 2) DASPMM_GO((KERN<T, CM, EXACT, V, W, 2>), p.grid, kThreads);           \
+    else DASPMM_GO((KERN<T, CM, EXACT, V, W, 1>), p.grid, kThreads);
 
 #define DASPMM_PR_W_TABLE(KERN, T, CM, EXACT, V)                                        \
     switch (p.L) {                                                                     \

@@ -9,14 +9,14 @@ namespace daspmm {
 // KERN is k_rb_sr or k_eb_sr.
 #define DASPMM_SR_LPR_TABLE(KERN, T, CM, EXACT, V)                                      \
     switch (p.L) {                                                                     \
-        case 1: KERN<T, CM, EXACT, V, 1, 1><<<p.grid, kThreads, 0, s>>>(a); break;     \
-        case 2: KERN<T, CM, EXACT, V, 2, 1><<<p.grid, kThreads, 0, s>>>(a); break;     \
-        case 4: KERN<T, CM, EXACT, V, 4, 1><<<p.grid, kThreads, 0, s>>>(a); break;     \
-        case 8: KERN<T, CM, EXACT, V, 8, 1><<<p.grid, kThreads, 0, s>>>(a); break;     \
-        case 16: KERN<T, CM, EXACT, V, 16, 1><<<p.grid, kThreads, 0, s>>>(a); break;   \
+        case 1: DASPMM_GO((KERN<T, CM, EXACT, V, 1, 1>), p.grid, kThreads); break;     \
+        case 2: DASPMM_GO((KERN<T, CM, EXACT, V, 2, 1>), p.grid, kThreads); break;     \
+        case 4: DASPMM_GO((KERN<T, CM, EXACT, V, 4, 1>), p.grid, kThreads); break;     \
+        case 8: DASPMM_GO((KERN<T, CM, EXACT, V, 8, 1>), p.grid, kThreads); break;     \
+        case 16: DASPMM_GO((KERN<T, CM, EXACT, V, 16, 1>), p.grid, kThreads); break;   \
         case 32:                                                                       \
-            if (p.X == 2) KERN<T, CM, EXACT, V, 32, 2><<<p.grid, kThreads, 0, s>>>(a); \
-            else KERN<T, CM, EXACT, V, 32, 1><<<p.grid, kThreads, 0, s>>>(a);          \
+            if (p.X == 2) DASPMM_GO((KERN<T, CM, EXACT, V, 32, 2>), p.grid, kThreads); \
+            else DASPMM_GO((KERN<T, CM, EXACT, V, 32, 1>), p.grid, kThreads);          \
             break;                                                                     \
         default: return cudaErrorNotSupported;                                         \
     }

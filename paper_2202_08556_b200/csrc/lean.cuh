@@ -148,10 +148,12 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
     auto deposit = [&](int row) {
         if (colok) {
             float* y = Ccol + int64_t(row) * a.ldc;
-            if ((first_split && row == r_first) || (last_split && row == r_last))
+            if ((first_split && row == r_first) || (last_split && row == r_last)) {
+                griddep_wait();  // split row: zeroed by the EB prologue
                 atomic_add_frag(y, acc);
-            else
+            } else {
                 st_frag(y, acc);
+            }
         }
 #pragma unroll
         for (int i = 0; i < V; ++i) acc.v[i] = 0.f;
@@ -234,7 +236,10 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_s
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
-    if (e0l >= a.nnz) return;
+    if (e0l >= a.nnz) {
+        griddep_wait();
+        return;
+    }
     const int e0 = int(e0l), e1 = int(min(a.nnz, e0l + a.sub));
     const int col = blockIdx.y * (LPR * V) + gl * V;
     const bool colok = col < a.N;
@@ -249,13 +254,18 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_s
         const Frag<float, V> acc = row_segment<V>(a, s, se, Bc, ldb_bytes, colok);
         if (colok) {
             float* y = a.C + int64_t(r) * a.ldc + col;
-            if (rs >= e0 && re <= e1) st_frag(y, acc);
-            else atomic_add_frag(y, acc);
+            if (rs >= e0 && re <= e1) {
+                st_frag(y, acc);
+            } else {
+                griddep_wait();
+                atomic_add_frag(y, acc);
+            }
         }
         s = se;
         if (s >= e1) break;
         r = __ldg(a.rows + s);
     }
+    griddep_wait();
 }
 
 // EB, range walk: the chunk as one nonzero range with COO row ids (range_walk). Suits
@@ -265,13 +275,17 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_s
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
-    if (e0l >= a.nnz) return;
+    if (e0l >= a.nnz) {
+        griddep_wait();
+        return;
+    }
     const int e0 = int(e0l), e1 = int(min(a.nnz, e0l + a.sub));
     const bool first_split = e0 > 0 && __ldg(a.rows + e0 - 1) == __ldg(a.rows + e0);
     const bool last_split = e1 < a.nnz && __ldg(a.rows + e1) == __ldg(a.rows + e1 - 1);
     const int col = blockIdx.y * (LPR * V) + gl * V;
     range_walk<V>(a, e0, e1, first_split, last_split, reinterpret_cast<const char*>(a.B + col),
                   int(a.ldb) * int(sizeof(float)), a.C + col, col < a.N);
+    griddep_wait();
 }
 
 }  // namespace daspmm

@@ -1,18 +1,19 @@
 // EB+SR launchers (K4 EB+RM+SR, K6 EB+CM+SR) and the EB partition/zeroing prologue.
+#define DASPMM_PDL_EXPR (p.pdl)
 #include "launch_sr.cuh"
 namespace daspmm {
 // Fast path instantiations (CTA-combined boundary rows); the exact path keeps one
 // partition chunk per group (k_eb_sr) so owned rows match the reference bit for bit.
 #define DASPMM_CTA_LPR_TABLE_NT(T, CM, V, NT)                                             \
     switch (p.L) {                                                                        \
-        case 1: k_eb_sr_cta<T, CM, V, 1, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
-        case 2: k_eb_sr_cta<T, CM, V, 2, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
-        case 4: k_eb_sr_cta<T, CM, V, 4, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
-        case 8: k_eb_sr_cta<T, CM, V, 8, 1, NT><<<p.grid, NT, 0, s>>>(a); break;          \
-        case 16: k_eb_sr_cta<T, CM, V, 16, 1, NT><<<p.grid, NT, 0, s>>>(a); break;        \
+        case 1: DASPMM_GO((k_eb_sr_cta<T, CM, V, 1, 1, NT>), p.grid, NT); break;          \
+        case 2: DASPMM_GO((k_eb_sr_cta<T, CM, V, 2, 1, NT>), p.grid, NT); break;          \
+        case 4: DASPMM_GO((k_eb_sr_cta<T, CM, V, 4, 1, NT>), p.grid, NT); break;          \
+        case 8: DASPMM_GO((k_eb_sr_cta<T, CM, V, 8, 1, NT>), p.grid, NT); break;          \
+        case 16: DASPMM_GO((k_eb_sr_cta<T, CM, V, 16, 1, NT>), p.grid, NT); break;        \
         case 32:                                                                          \
-            if (p.X == 2) k_eb_sr_cta<T, CM, V, 32, 2, NT><<<p.grid, NT, 0, s>>>(a);      \
-            else k_eb_sr_cta<T, CM, V, 32, 1, NT><<<p.grid, NT, 0, s>>>(a);               \
+            if (p.X == 2) DASPMM_GO((k_eb_sr_cta<T, CM, V, 32, 2, NT>), p.grid, NT);      \
+            else DASPMM_GO((k_eb_sr_cta<T, CM, V, 32, 1, NT>), p.grid, NT);               \
             break;                                                                        \
         default: return cudaErrorNotSupported;                                            \
     }
@@ -49,9 +50,9 @@ DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
 template <int NT>
 static cudaError_t launch_eb_sr_thr_nt(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
     switch (p.V) {
-        case 1: k_eb_sr_thr<float, false, 1, kThrS, NT><<<p.grid, NT, 0, s>>>(a); break;
-        case 2: k_eb_sr_thr<float, false, 2, kThrS, NT><<<p.grid, NT, 0, s>>>(a); break;
-        case 4: k_eb_sr_thr<float, false, 4, kThrS4, NT><<<p.grid, NT, 0, s>>>(a); break;
+        case 1: DASPMM_GO((k_eb_sr_thr<float, false, 1, kThrS, NT>), p.grid, NT); break;
+        case 2: DASPMM_GO((k_eb_sr_thr<float, false, 2, kThrS, NT>), p.grid, NT); break;
+        case 4: DASPMM_GO((k_eb_sr_thr<float, false, 4, kThrS4, NT>), p.grid, NT); break;
         default: return cudaErrorNotSupported;
     }
     return cudaGetLastError();

@@ -1,4 +1,5 @@
 // Launchers of the lean SR kernels (lean.cuh): RB+RM+SR and EB+RM+SR, fp32 fast mode.
+#define DASPMM_PDL_EXPR (p.pdl && p.kernel >= 4)
 #include "dispatch.h"
 #include "lean.cuh"
 
@@ -6,12 +7,12 @@ namespace daspmm {
 
 #define DASPMM_LEAN_LPR_NT(KERN, V, NT)                                               \
     switch (p.L) {                                                                   \
-        case 1: KERN<V, 1, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
-        case 2: KERN<V, 2, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
-        case 4: KERN<V, 4, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
-        case 8: KERN<V, 8, NT><<<p.grid, NT, 0, s>>>(a); break;                      \
-        case 16: KERN<V, 16, NT><<<p.grid, NT, 0, s>>>(a); break;                    \
-        case 32: KERN<V, 32, NT><<<p.grid, NT, 0, s>>>(a); break;                    \
+        case 1: DASPMM_GO((KERN<V, 1, NT>), p.grid, NT); break;                      \
+        case 2: DASPMM_GO((KERN<V, 2, NT>), p.grid, NT); break;                      \
+        case 4: DASPMM_GO((KERN<V, 4, NT>), p.grid, NT); break;                      \
+        case 8: DASPMM_GO((KERN<V, 8, NT>), p.grid, NT); break;                      \
+        case 16: DASPMM_GO((KERN<V, 16, NT>), p.grid, NT); break;                    \
+        case 32: DASPMM_GO((KERN<V, 32, NT>), p.grid, NT); break;                    \
         default: return cudaErrorNotSupported;                                       \
     }
 #define DASPMM_LEAN_LPR(KERN, V)                                                      \

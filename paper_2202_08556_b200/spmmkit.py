@@ -38,7 +38,7 @@ __all__ = [
     "convert_layout", "DeviceCsr", "spmm", "spmm_auto_layout", "spmm_device",
     "extract_features", "FeatureVector", "partition_elements", "SelectorModel", "load_selector",
     "predict_kernel", "Tolerance", "tolerance_equal", "InvalidArgument", "OutOfRange",
-    "ModelFormatError",
+    "ModelFormatError", "spmm_selected", "SpmmBatch", "selected_cache_info",
 ]
 
 
@@ -554,6 +554,38 @@ def spmm_selected(a: DeviceCsr, model: SelectorModel, B, C_out, b_layout=Layout.
                                      C_out.data_ptr(), _ld(C_out), W, flags, kp,
                                      _stream_ptr(stream)))
     return C_out
+
+
+class SpmmBatch:
+    """Many independent DA-SpMM calls launched as ONE CUDA graph.
+
+    ``calls`` is a list of (DeviceCsr, B, C_out) (row-major, as spmm_selected). Each call
+    runs once eagerly so the device publishes its selection; the batch is then captured
+    (only the chosen kernels' launches, EB prologues included) and every ``run()`` is one
+    graph launch — the per-call host path and launch latency are paid once per batch
+    (small matrices: a few microseconds of kernel each). Operands are bound at capture:
+    refill the same B / C tensors between runs."""
+
+    def __init__(self, calls, model: "SelectorModel", W: int = 8, hw: int = -1):
+        import torch
+
+        self.calls = list(calls)
+        for d, B, Cc in self.calls:
+            spmm_selected(d, model, B, Cc, W=W, hw=hw)
+        torch.cuda.synchronize()
+        for d, B, Cc in self.calls:  # decisions are published: the direct launches
+            spmm_selected(d, model, B, Cc, W=W, hw=hw)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(self.graph, stream=side):
+            for d, B, Cc in self.calls:
+                spmm_selected(d, model, B, Cc, W=W, hw=hw)
+        torch.cuda.current_stream().wait_stream(side)
+
+    def run(self):
+        self.graph.replay()
 
 
 def selected_cache_info(a: DeviceCsr):
