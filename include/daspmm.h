@@ -111,7 +111,9 @@ int daspmm_csr_device_arrays(const daspmm_csr* csr, const int32_t** d_row_offset
 /* spmm() — spmm.hpp:194-271, device-resident operands.
  *   kernel      0..7, KernelId::index() = 4m + 2n + k (kernel_id.hpp:25-27)
  *   P, W, Cb    WorkerConfig (worker.hpp:18-40): validated as the reference does
- *               (P >= 1 or 0 = library choice, W power of two in [2, 32], Cb >= 1).
+ *               (P >= 1 or 0 = library choice, W power of two in [2, 1024], Cb >= 1;
+ *               W > 32 runs one CTA of W threads per group — the reference accepts any
+ *               power of two, widths above 1024 return DASPMM_ERR_UNSUPPORTED).
  *               W is the PR reduction width; P the EB chunk count when honoured
  *               (P > 0, or always in DASPMM_EXACT mode); Cb does not change results.
  *   d_B         K x N operand; b_layout must equal the kernel's N-loop choice

@@ -53,10 +53,10 @@ static int validate_config(int64_t P, int64_t W, int64_t Cb, bool allow_auto_p) 
         bad = true;
     }
     if (bad) return fail(DASPMM_ERR_INVALID_CONFIG, msg);
-    if (W > 32)
+    if (W > 1024)
         return fail(DASPMM_ERR_UNSUPPORTED,
                     "spmm: group_width " + std::to_string(W) +
-                        " exceeds the 32-lane warp (B200 build supports 2..32)");
+                        " exceeds one 1024-thread CTA (B200 build supports 2..1024)");
     return DASPMM_OK;
 }
 
@@ -299,6 +299,14 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         p.X = nv > 32 ? 2 : 1;
         tile_cols = int64_t(p.L) * p.V * p.X;
         lanes = p.L;
+    } else if (W > 32) {
+        // wider than a warp: one CTA of W threads per group, scalar columns
+        // (spmm_pr_wide.cu); the group walks every column itself, so one column tile.
+        p.L = int(W);
+        p.V = 1;
+        p.X = 1;
+        tile_cols = std::max<int64_t>(N, 1);
+        lanes = p.L;
     } else {
         p.L = int(W);
         p.X = nv > W ? 2 : 1;
@@ -474,6 +482,15 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
             }
             return launch_sr_lean(p, a, s);
         }
+    }
+    if (pr && p.L > 32) {  // group wider than a warp (spmm_pr_wide.cu)
+        if (eb) {
+            cudaError_t e = launch_eb_prep<T>(h->rp, int(h->M), h->nnz, p.P, chunk_row,
+                                              static_cast<T*>(C), ldc, int(N), h->empty_rows,
+                                              int(h->n_empty), h->coo_rows, s);
+            if (e != cudaSuccess) return e;
+        }
+        return launch_pr_wide<T>(p, a, s);
     }
     if (eb) {
         cudaError_t e =

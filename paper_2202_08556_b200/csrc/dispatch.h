@@ -90,6 +90,8 @@ template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, 
 template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+// PR groups wider than a warp (W = 64 .. 1024), RB and EB (spmm_pr_wide.cu).
+template <typename T> cudaError_t launch_pr_wide(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T>
 cudaError_t launch_eb_prep_uniform(const int* rows, int64_t nnz, int64_t sub, int64_t n_sub, int G,
                                    T* C, int64_t ldc, int N, const int* empty_rows, int n_empty,

@@ -746,3 +746,44 @@ def test_fault_injection_is_caught(sk):
         del os.environ["SPMMKIT_ENABLE_FAULT_INJECTION"], os.environ["DASPMM_INJECT_FAULT"]
         sk.reload_env()
     assert run()
+
+
+@pytest.mark.parametrize("W", [64, 128, 256, 1024])
+def test_pr_group_width_above_a_warp(sk, W):
+    """worker.hpp:29-40 accepts any power-of-two group width: W > 32 runs one CTA of W
+    threads per group (spmm_pr_wide.cu). Exact mode against the oracle's restatement of
+    the reference worker (pinned to the reference on golden): RB+PR bit-identical (the
+    W-lane tree = warp trees + tree over warp totals), EB+PR bit-identical on rows owned
+    by one chunk; fast mode within the gamma bound."""
+    import torch
+
+    cases = [H.csr_from_counts([6, 2, 0, 3, 1, 300, 0, 2000, 5], 2100),
+             H.random_csr(400, 900, 30000, seed=W, skew=1.5)]
+    for a in cases:
+        for dt in (np.float64, np.float32):
+            ad = a.astype(dt)
+            d = sk.DeviceCsr.from_host(ad)
+            for n in (1, 3, 33):
+                x = np.random.default_rng(n + W).uniform(-1, 1, (a.num_cols, n))
+                for k in (1, 3, 5, 7):
+                    P = 3
+                    xd = sk.DenseMatrix.from_logical(x.astype(dt), sk.Layout.ColMajor if k & 2
+                                                     else sk.Layout.RowMajor)
+                    y = sk.spmm(sk.KernelId.from_index(k), d, xd, sk.WorkerConfig(P, W, 2),
+                                exact=True).logical()
+                    want = O.spmm_kernel(k, H.to_oracle(ad), x.astype(dt), P=P, W=W, Cb=2,
+                                         dtype=dt)
+                    if k < 4:
+                        np.testing.assert_array_equal(y, want, err_msg=f"k{k} W{W} n{n} {dt}")
+                    else:
+                        shared = H.split_rows(ad, P)
+                        np.testing.assert_array_equal(y[~shared], want[~shared])
+                        np.testing.assert_allclose(y, want, rtol=1e-3 if dt == np.float32 else 1e-10,
+                                                   atol=1e-6 if dt == np.float32 else 1e-12)
+                    yf = sk.spmm(sk.KernelId.from_index(k), d, xd, sk.WorkerConfig(1, W, 2)).logical()
+                    bound = H.gamma_bound(ad, x.astype(dt), dt)
+                    y64 = O.spmm_reference(H.to_oracle(ad), x.astype(dt).astype(np.float64))
+                    assert (np.abs(yf.astype(np.float64) - y64) <= bound).all(), (k, W, n)
+    with pytest.raises(RuntimeError, match="supports 2..1024"):
+        sk.spmm(sk.KernelId.from_index(1), cases[0], sk.DenseMatrix.zeros(2100, 2),
+                sk.WorkerConfig(1, 2048, 2))
