@@ -151,10 +151,47 @@ def build_suite(small: bool, rank: int, world: int, workload: str = "suite"):
     mats = []
     for name, mk, ns in gen.workload(workload, small=small):
         M, K, rp, ci, va = mk()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         full = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+        torch.cuda.synchronize()
+        t_handle = (time.perf_counter() - t0) * 1e3
         mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), full=full,
-                         rp=rp, ci=ci, va=va, ns=ns))
+                         rp=rp, ci=ci, va=va, ns=ns, handle_ms=t_handle))
     return mats
+
+
+def _setup_costs(mats):
+    """Handle-creation cost per matrix (not in any timed SpMM): device arrays adopted
+    (features, empty rows, K_touched, column windows: daspmm_csr_create_device), host int64
+    arrays uploaded and validated / compacted on the device (daspmm_csr_create_host), the
+    COO row ids built on first EB use, and extract_features' exact std_row replay."""
+    import numpy as np
+    import torch
+
+    from paper_2202_08556_b200 import spmmkit as sk
+
+    out = {}
+    for m in mats:
+        rp = m["rp"].cpu().numpy().astype(np.int64)
+        ci = m["ci"].cpu().numpy().astype(np.int64)
+        va = m["va"].cpu().numpy()
+        a = sk.CsrMatrix(m["M"], m["K"], rp, ci, va, np.float32)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = sk.DeviceCsr.from_host(a)
+        torch.cuda.synchronize()
+        t_host = (time.perf_counter() - t0) * 1e3
+        t0 = time.perf_counter()
+        sk.extract_features(h, 32)
+        t_feat = (time.perf_counter() - t0) * 1e3
+        h.close()
+        out[m["name"]] = {"from_device_ms": round(m.get("handle_ms", 0.0), 3),
+                          "from_host_ms": round(t_host, 3),
+                          "extract_features_exact_ms": round(t_feat, 3),
+                          "rows": m["M"], "nnz": m["nnz_total"]}
+        del a, rp, ci, va
+    return out
 
 
 def shard_calls(mats, ns_override, rank: int, world: int):
@@ -307,6 +344,7 @@ def run_ours(args):
     warm = _warm(calls, one, stream, world, dev, total_flops)
     overhead = _da_overhead(calls, model, stream, flush) if rank == 0 else None
     batched = _batched_small(calls, model, flush, per_call_ms) if rank == 0 else None
+    setup = _setup_costs(mats) if rank == 0 and world == 1 else None
     assembly = None
     if world > 1:
         try:
@@ -317,7 +355,7 @@ def run_ours(args):
         _write_roofline_table(args.roofline_table, calls, per_call_ms, chosen, peak)
     return _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
                    per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-                   flush, assembly, warm, overhead, batched)
+                   flush, assembly, warm, overhead, batched, setup)
 
 
 def _batched_small(calls, model, flush, per_call_ms, reps=5, max_nnz=300_000):
@@ -577,7 +615,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
 
 def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches_per_step,
             per_call_ms, dom, dom_ach, achieved, peak, peak_kind, traffic, clk, e2e, parity,
-            flush, assembly=None, warm=None, overhead=None, batched=None):
+            flush, assembly=None, warm=None, overhead=None, batched=None, setup=None):
     import torch.distributed as dist
 
     from paper_2202_08556_b200 import spmmkit as sk
@@ -624,6 +662,7 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
         "warm_l2": warm,
         "da_spmm_overhead": overhead,
         "small_calls_batched": batched,
+        "setup_cost": setup,
     }
     if assembly is not None:
         result["assembly"] = assembly

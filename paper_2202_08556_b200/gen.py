@@ -55,7 +55,17 @@ def rmat(scale: int, nnz: int, a=0.25, b=0.25, c=0.25, d=0.25, seed: int = 0,
          dtype=torch.float32, device="cuda", crop: int | None = None):
     """R-MAT with ~nnz distinct cells (draws in batches until the target is met or
     the reference's 10x draw cap is hit, rmat.hpp:52-76)."""
-    assert abs(a + b + c + d - 1.0) < 1e-9
+    # parameter checks and the draw-cap contract of rmat.hpp:22-36, 77-80
+    if scale < 0 or scale > 30:
+        raise ValueError("rmat: scale must be in [0, 30]")
+    if any(q < 0.0 or q > 1.0 for q in (a, b, c, d)):
+        raise ValueError("rmat: quadrant probabilities must be in [0, 1]")
+    if abs(a + b + c + d - 1.0) > 1e-9:
+        raise ValueError("rmat: quadrant probabilities must sum to 1")
+    if nnz < 0:
+        raise ValueError("rmat: target_nnz must be nonnegative")
+    if nnz > (crop or (1 << scale)) ** 2:
+        raise ValueError("rmat: target_nnz exceeds 2^(2*scale) cells")
     dim = 1 << scale
     M = K = crop or dim
     g = torch.Generator(device=device)
@@ -71,6 +81,8 @@ def rmat(scale: int, nnz: int, a=0.25, b=0.25, c=0.25, d=0.25, seed: int = 0,
         drawn += need
         keys = torch.unique(torch.cat([keys, r * K + cc]))
         del r, cc
+    if keys.numel() < 0.99 * nnz:
+        raise RuntimeError(f"rmat: draw cap exhausted at {keys.numel()} of {nnz} target nonzeros")
     if keys.numel() > nnz:  # keep a uniformly random subset of exactly nnz cells
         perm = torch.randperm(keys.numel(), generator=g, device=device)[:nnz]
         keys = torch.sort(keys[perm]).values
