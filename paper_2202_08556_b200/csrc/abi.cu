@@ -7,6 +7,8 @@
 #include <cstring>
 #include <string>
 
+#include <chrono>
+
 #include "dispatch.h"
 #include "internal.h"
 #include "kernels.cuh"
@@ -20,6 +22,16 @@ static bool debug_on() {
     return on;
 }
 void set_error(const std::string& msg) { g_err = msg; }
+
+// DASPMM_DEBUG also traces handle creation: wall time since the previous mark.
+void trace_mark(const char* what) {
+    if (!debug_on()) return;
+    static thread_local std::chrono::steady_clock::time_point last;
+    const auto now = std::chrono::steady_clock::now();
+    if (what) fprintf(stderr, "[daspmm] %-28s %9.3f ms\n", what,
+                      std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
 int fail(int code, const std::string& msg) {
     g_err = msg;
     if (debug_on()) fprintf(stderr, "[daspmm] error %d: %s\n", code, msg.c_str());
@@ -664,6 +676,7 @@ cudaError_t ingest(const int64_t* rp, const int64_t* ci, int64_t M, int64_t K, i
     if (e == cudaSuccess) e = cudaMemcpy(d64, rp, sizeof(int64_t) * n_rp, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && n_ci > 0)
         e = cudaMemcpy(d64 + n_rp, ci, sizeof(int64_t) * n_ci, cudaMemcpyHostToDevice);
+    trace_mark("ingest: malloc+h2d int64");
     if (e == cudaSuccess) {
         const int64_t n = std::max<int64_t>(M + 1, nnz);
         const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 32));
@@ -672,8 +685,10 @@ cudaError_t ingest(const int64_t* rp, const int64_t* ci, int64_t M, int64_t K, i
     }
     unsigned long long hb[2] = {~0ull, ~0ull};
     if (e == cudaSuccess) e = cudaMemcpy(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost);
+    trace_mark("ingest: k_ingest+d2h");
     cudaFree(d64);
     cudaFree(d_bad);
+    trace_mark("ingest: free");
     for (int i = 0; i < 2; ++i)
         bad_out[i] = hb[i] == ~0ull ? INT64_MAX : int64_t(hb[i]);
     return e;
@@ -699,6 +714,7 @@ int daspmm_device_count(void) {
 
 static int finish_create(daspmm_csr* h, cudaStream_t s, daspmm_csr** out) {
     int rc = compute_features(h, s);
+    trace_mark("create: features+spans");
     if (rc) {
         daspmm_csr_destroy(h);
         return rc;
@@ -727,6 +743,7 @@ int daspmm_csr_create_host(int64_t M, int64_t K, int64_t nnz, const int64_t* rp,
         cudaGetLastError();
         return fail(DASPMM_ERR_CUDA, "csr_create: no CUDA device (daspmm has no CPU fallback)");
     }
+    trace_mark(nullptr);
     daspmm_csr* h = new daspmm_csr;
     h->M = M;
     h->K = K;
@@ -741,12 +758,14 @@ int daspmm_csr_create_host(int64_t M, int64_t K, int64_t nnz, const int64_t* rp,
         daspmm_csr_destroy(h);
         return cuda_fail(e, "csr_create: cudaMalloc");
     }
+    trace_mark("create_host: malloc");
     int64_t bad[2] = {INT64_MAX, INT64_MAX};
     if ((e = ingest(rp, ci, M, K, nnz, h->rp, h->ci, bad)) != cudaSuccess ||
         (nnz > 0 && (e = cudaMemcpy(h->va, values, es * nnz, cudaMemcpyHostToDevice)) != cudaSuccess)) {
         daspmm_csr_destroy(h);
         return cuda_fail(e, "csr_create: upload");
     }
+    trace_mark("create_host: ingest+values");
     std::string msg;
     if (bad[0] != INT64_MAX)
         msg = "csr_create: row_offsets nondecreasing violated at index " + std::to_string(bad[0]);

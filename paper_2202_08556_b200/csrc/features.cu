@@ -216,6 +216,7 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
     if (M > 0) cudaMemcpyAsync(hp.data(), partial, sizeof(double) * blocks, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
+    trace_mark("features: kernels+sync");
     cudaFree(partial);
     cudaFree(counters);
     cudaFree(bitmap);
@@ -246,6 +247,7 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
                              s)) != cudaSuccess)
         return cuda_fail(e, "cudaMemcpy(features)");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
+    trace_mark("features: host interval");
     return compute_spans(h, s);
 }
 

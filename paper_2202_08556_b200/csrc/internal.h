@@ -27,6 +27,7 @@ struct DevFeatures {
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
+void trace_mark(const char* what);  // DASPMM_DEBUG timing trace (nullptr resets)
 int cuda_fail(cudaError_t e, const char* what);
 
 struct DeviceGuard {

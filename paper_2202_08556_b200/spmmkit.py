@@ -563,10 +563,14 @@ class SpmmBatch:
     runs once eagerly so the device publishes its selection; the batch is then captured
     (only the chosen kernels' launches, EB prologues included) and every ``run()`` is one
     graph launch — the per-call host path and launch latency are paid once per batch
-    (small matrices: a few microseconds of kernel each). Operands are bound at capture:
+    (small matrices: a few microseconds of kernel each). The calls are captured on
+    ``branches`` parallel graph branches (forked from and joined to the capture stream),
+    so small calls that each fill a fraction of the 148 SMs run side by side; calls that
+    write the same C stay on one branch, in list order. Operands are bound at capture:
     refill the same B / C tensors between runs."""
 
-    def __init__(self, calls, model: "SelectorModel", W: int = 8, hw: int = -1):
+    def __init__(self, calls, model: "SelectorModel", W: int = 8, hw: int = -1,
+                 branches: int = 8):
         import torch
 
         self.calls = list(calls)
@@ -576,12 +580,27 @@ class SpmmBatch:
         for d, B, Cc in self.calls:  # decisions are published: the direct launches
             spmm_selected(d, model, B, Cc, W=W, hw=hw)
         torch.cuda.synchronize()
+        nb = max(1, min(int(branches), len(self.calls)))
+        owner = {}  # C address -> branch, so writes to one C keep their order
+        lanes = [[] for _ in range(nb)]
+        for i, (d, B, Cc) in enumerate(self.calls):
+            b = owner.setdefault(Cc.data_ptr(), len(owner) % nb)
+            lanes[b].append((d, B, Cc))
+        self.branches = sum(1 for ln in lanes if ln)
         self.graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
+        forks = [torch.cuda.Stream() for _ in range(nb)]
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.graph(self.graph, stream=side):
-            for d, B, Cc in self.calls:
-                spmm_selected(d, model, B, Cc, W=W, hw=hw)
+            for f, ln in zip(forks, lanes):
+                if not ln:
+                    continue
+                f.wait_stream(side)
+                for d, B, Cc in ln:
+                    spmm_selected(d, model, B, Cc, W=W, hw=hw, stream=f)
+            for f, ln in zip(forks, lanes):
+                if ln:
+                    side.wait_stream(f)
         torch.cuda.current_stream().wait_stream(side)
 
     def run(self):

@@ -239,3 +239,35 @@ def test_spmm_batch_graph_replays_selected_kernels(env):
         y64 = O.spmm_reference(H.to_oracle(a), x64)
         err = np.abs(Cc.cpu().numpy().astype(np.float64) - y64)
         assert (err <= H.gamma_bound(a, x64, np.float32)).all()
+
+
+def test_spmm_batch_branches_keep_same_output_order(env):
+    """SpmmBatch on parallel graph branches: two calls that write the same C stay on one
+    branch in list order (the later call's result is what remains), the other calls run
+    beside them; one branch and eight branches give identical bits."""
+    torch, gen, sk, model = env
+    a = H.random_csr(3000, 2500, 40000, seed=77, skew=0.8)
+    b2 = H.random_csr(2000, 2500, 30000, seed=78, skew=0.0)
+    d, d2 = _dev(env, a), _dev(env, b2)
+    B1 = torch.rand(a.num_cols, 16, device="cuda")
+    B2 = torch.rand(a.num_cols, 16, device="cuda") - 2.0
+    Cs = torch.full((a.num_rows, 16), float("nan"), device="cuda")
+    others = [(d2, torch.rand(b2.num_cols, n, device="cuda"),
+               torch.full((b2.num_rows, n), float("nan"), device="cuda")) for n in (4, 32, 64)]
+    calls = [(d, B1, Cs)] + others + [(d, B2, Cs)]
+    outs = []
+    for nb in (1, 8):
+        batch = sk.SpmmBatch(calls, model, branches=nb)
+        for _, _, c in calls:
+            c.fill_(float("nan"))
+        batch.run()
+        torch.cuda.synchronize()
+        outs.append([c.clone() for _, _, c in calls])
+        assert batch.branches == (1 if nb == 1 else 4)
+    want = [(a, B2)] + [(b2, B) for _, B, _ in others] + [(a, B2)]
+    for res in outs:
+        for (m, B), y in zip(want, res):
+            x64 = B.cpu().numpy().astype(np.float64)
+            y64 = O.spmm_reference(H.to_oracle(m), x64)
+            err = np.abs(y.cpu().numpy().astype(np.float64) - y64)
+            assert (err <= H.gamma_bound(m, x64, np.float32)).all()
