@@ -278,14 +278,17 @@ def run_ours(args):
                           bytes=gen.algorithmic_bytes(d.num_rows, d.nnz(), w, d.cols_touched)))
     stream = torch.cuda.current_stream(dev)
 
-    def one(c):
-        sk.spmm_selected(c["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream)
+    def one(c, report=False):
+        # the optional kernel-id output costs a small H2D copy per call (~4 us after an
+        # L2 flush), so only the untimed warm-up asks for it
+        sk.spmm_selected(c["d"], model, c["B"], c["C"], kernel_out=c["kout"] if report else None,
+                         stream=stream)
 
     def step(times=None):
         for i, c in enumerate(calls):
             _flush(flush)
             if times is None:
-                one(c)
+                one(c, report=True)
             else:
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
@@ -601,7 +604,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
 
     e2e_step(first=True)
     torch.cuda.synchronize()
-    e2e_steps = max(1, min(args.steps, 3 if args.workload == "suite" else 1))
+    e2e_steps = max(1, min(args.steps, 5 if args.workload == "suite" else 1))
     if world > 1:
         import torch.distributed as dist
 
@@ -624,7 +627,7 @@ def _e2e(calls, one, stream, args, world, total_flops):
             "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
             "pcie": bound,
             "pipeline": "H2D stream -> DA-SpMM on the compute stream -> D2H stream, "
-                        "3 steps back to back"}
+                        f"{e2e_steps} steps back to back"}
 
 
 def _pcie_bound_ms(dev, h2d, d2h, mb=512):
@@ -718,7 +721,7 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
         result["cusparse"] = _cusparse_compare(calls, flush, per_call_ms, ns)
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = _cpu_baseline(
-            mats, [int(n) for n in args.ns.split(",")] if args.ns else None, steps=1)
+            mats, [int(n) for n in args.ns.split(",")] if args.ns else None)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -873,14 +876,15 @@ def _cusparse_compare(calls, flush, our_ms, ns, reps=5):
 
 
 # ------------------------------------------------------------------ CPU reference
-REF_PANEL_NNZ = 4_000_000
+# Matrices above this many nonzeros are represented by a middle row panel of that size in
+# the CPU arm (rows are independent in spmm, spmm.hpp:23-30, so a panel's GFLOP/s is the
+# matrix's). It keeps c5 (503M nnz: ~75 GB of host CSR + X + Y) bounded; every matrix of
+# the suite, c1, c3 and c4 runs whole.
+REF_PANEL_NNZ = 150_000_000
 
 
 def _ref_sample(mats, ns_override=None):
-    """The CPU reference's sample: every (matrix, N) pair of the workload. Matrices
-    above REF_PANEL_NNZ nonzeros are represented by a middle row panel of about that
-    many nonzeros (rows are independent in spmm, spmm.hpp:23-30, so a panel's
-    GFLOP/s is the matrix's), keeping one pass to a few seconds of CPU work."""
+    """The CPU reference's unit of work: every (matrix, N) pair of the workload."""
     return [(m, n) for m in mats for n in (ns_override or m["ns"])]
 
 
@@ -897,65 +901,89 @@ def _ref_panel(m):
     return r0, max(r1, r0 + 1)
 
 
-def _cpu_time_reference(sample, steps):
-    """Times the reference's spmm() (RB+RM+SR, P = all host cores) via oracle/_ref."""
-    import numpy as np
+class _RefArm:
+    """The reference's own spmm() (RB+RM+SR, P = all host cores, oracle/_ref) over the
+    workload: reference CSR handles (int64, built once) and X operands (laid out once,
+    as time_kernel does, bench.hpp:125-137); one pass = one spmm() call per (matrix, N)
+    pair, each timed alone (wall clock around exactly the call, result dropped)."""
 
-    from oracle import oracle as O
+    def __init__(self, mats, ns_override=None):
+        import numpy as np
 
-    R = O.ref()
-    if R is None:
-        return None
-    cores = os.cpu_count() or 1
-    handles = {}
-    tot_flops = 0
-    tot_s = 0.0
-    panel_nnz = {}
-    for m, n in sample:
-        if m["name"] not in handles:
-            r0, r1 = _ref_panel(m)
-            rp = m["rp"].cpu().numpy().astype(np.int64)
-            s, e = int(rp[r0]), int(rp[r1])
-            ci = m["ci"][s:e].cpu().numpy().astype(np.int64)
-            va = m["va"][s:e].cpu().numpy().astype(np.float64)
-            handles[m["name"]] = R.ref_csr_from_csr(r1 - r0, m["K"], rp[r0:r1 + 1] - s, ci, va)
-            panel_nnz[m["name"]] = e - s
-        h = handles[m["name"]]
-        x = np.random.default_rng(n).uniform(-1, 1, (m["K"], n)).astype(np.float32).reshape(-1)
-        med, mn, ck = C.c_double(), C.c_double(), C.c_double()
-        rc = R.ref_time_spmm_f32(h, 0, cores, 8, 8, x, n, 7, 2, C.byref(med), C.byref(mn),
-                                 C.byref(ck))
-        if rc:
-            raise RuntimeError(R.ref_last_error().decode())
-        tot_s += med.value
-        tot_flops += 2 * panel_nnz[m["name"]] * n
-    for h in handles.values():
-        R.ref_csr_free(h)
-    return tot_flops / tot_s / 1e9, cores, tot_s
+        from oracle import oracle as O
+
+        self.R = O.ref()
+        self.cores = os.cpu_count() or 1
+        self.handles, self.dense, self.pairs = {}, [], []
+        self.panelled = []
+        if self.R is None:
+            return
+        R = self.R
+        for m, n in _ref_sample(mats, ns_override):
+            if m["name"] not in self.handles:
+                r0, r1 = _ref_panel(m)
+                if (r0, r1) != (0, m["M"]):
+                    self.panelled.append(m["name"])
+                rp = m["rp"].cpu().numpy().astype(np.int64)
+                s, e = int(rp[r0]), int(rp[r1])
+                ci = m["ci"][s:e].cpu().numpy().astype(np.int64)
+                va = m["va"][s:e].cpu().numpy().astype(np.float64)
+                self.handles[m["name"]] = (R.ref_csr_from_csr(r1 - r0, m["K"], rp[r0:r1 + 1] - s,
+                                                              ci, va), e - s)
+                del rp, ci, va
+            h, nnz = self.handles[m["name"]]
+            x = np.random.default_rng(n).uniform(-1, 1, (m["K"], n)).astype(np.float32)
+            d = R.ref_dense_f32(x.reshape(-1), m["K"], n, 0)
+            del x
+            self.dense.append(d)
+            self.pairs.append((h, d, 2 * nnz * n))
+        self.flops = sum(f for _, _, f in self.pairs)
+
+    def one_pass(self) -> float:
+        """Seconds of reference spmm() time for one pass over the workload."""
+        secs = C.c_double()
+        tot = 0.0
+        for h, d, _ in self.pairs:
+            if self.R.ref_time_spmm_once_f32(h, d, 0, self.cores, 8, 8, C.byref(secs)):
+                raise RuntimeError(self.R.ref_last_error().decode())
+            tot += secs.value
+        return tot
+
+    def close(self):
+        if self.R is None:
+            return
+        for d in self.dense:
+            self.R.ref_dense_free(d)
+        for h, _ in self.handles.values():
+            self.R.ref_csr_free(h)
+        self.dense, self.handles = [], {}
 
 
-def _cpu_baseline(mats, ns_override=None, steps=1):
-    sample = _ref_sample(mats, ns_override)
-    r = _cpu_time_reference(sample, steps)
-    if r is None:
+def _cpu_baseline(mats, ns_override=None, passes=3):
+    arm = _RefArm(mats, ns_override)
+    if arm.R is None:
         return {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
-    v, cores, secs = r
-    return {"value": round(v, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-            "sample": f"reference spmm() RB+RM+SR fp32, P={cores} threads, time_kernel_fn "
-                      f"(warmup 2, reps 7, median; bench.hpp:63-121) over all {len(sample)} (matrix, N) pairs of the "
-                      f"workload (matrices > {REF_PANEL_NNZ} nnz as a middle row panel of that "
-                      f"size); {secs:.2f} s of timed CPU work per pass"}
+    arm.one_pass()  # warm-up (first touch of X, the pool's threads)
+    secs = sorted(arm.one_pass() for _ in range(passes))[passes // 2]
+    v = arm.flops / secs / 1e9
+    arm.close()
+    whole = "every matrix whole" if not arm.panelled else \
+        f"{', '.join(arm.panelled)} as a middle row panel of {REF_PANEL_NNZ} nnz"
+    return {"value": round(v, 4), "unit": "GFLOP/s", "cores": arm.cores, "kind": "reference",
+            "sample": f"reference spmm() RB+RM+SR fp32, P={arm.cores} threads, one call per "
+                      f"(matrix, N) pair of the workload ({len(arm.pairs)} pairs, {whole}); "
+                      f"median of {passes} passes of {secs:.2f} s"}
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU implementation alone (rank 0)."""
+    """--impl reference: the reference CPU implementation alone (rank 0): every step is one
+    pass of the reference's spmm() over the same workload as our arm's step."""
     world, rank, local = _dist()
     if rank != 0:
         return
     import torch
 
-    ns = [int(n) for n in args.ns.split(",")] if args.ns else list(NS)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     if dev == "cuda":
         torch.cuda.set_device(local)
@@ -966,35 +994,37 @@ def run_reference(args):
         M, K, rp, ci, va = mk()
         mats.append(dict(name=name, M=M, K=K, nnz_total=int(ci.numel()), rp=rp, ci=ci, va=va,
                          ns=wns))
-    sample = _ref_sample(mats, [int(n) for n in args.ns.split(",")] if args.ns else None)
-    from oracle import oracle as O
-
-    if O.ref() is None:
+    ns_override = [int(n) for n in args.ns.split(",")] if args.ns else None
+    ns = sorted({n for m in mats for n in (ns_override or m["ns"])})
+    arm = _RefArm(mats, ns_override)
+    if arm.R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built here"}))
         return
+    for m in mats:  # generated operands are no longer needed on the device
+        m["rp"] = m["ci"] = m["va"] = None
     for _ in range(args.warmup):
-        _cpu_time_reference(sample[:1], 1)
-    vals, secs = [], 0.0
-    cores = os.cpu_count() or 1
-    for _ in range(args.steps):
-        v, cores, s = _cpu_time_reference(sample, 1)
-        vals.append(v)
-        secs += s
-    value = statistics.median(vals)
+        arm.one_pass()
+    step_s = [arm.one_pass() for _ in range(max(args.steps, 1))]
+    secs = statistics.median(step_s)
+    value = arm.flops / secs / 1e9
+    whole = "every matrix whole" if not arm.panelled else \
+        f"{', '.join(arm.panelled)} as a middle row panel of {REF_PANEL_NNZ} nnz"
+    arm.close()
     out = {"impl": "reference",
            "metric": "SpMM GFLOP/s (2*nnz*N/t), DA-SpMM over the synthetic suite",
            "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(secs / max(args.steps, 1) * 1e3, 3),
+           "warmup": args.warmup, "ms_per_step": round(secs * 1e3, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic",
-           "config": {"workload": f"{args.workload} (reference CPU; matrices above "
-                                  f"{REF_PANEL_NNZ} nnz as a middle row panel)", "ns": ns},
+           "config": {"workload": f"{args.workload} (reference CPU, {whole})", "ns": ns,
+                      "calls_per_step": len(arm.pairs)},
            "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
-           "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
+           "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": arm.cores,
                             "kind": "reference",
-                            "sample": f"reference spmm() RB+RM+SR fp32, P={cores}, "
-                                      f"{len(sample)} (matrix, N) pairs per step"}}
+                            "sample": f"reference spmm() RB+RM+SR fp32, P={arm.cores} threads, "
+                                      f"one pass over {len(arm.pairs)} (matrix, N) pairs per "
+                                      f"step ({whole}), median over steps"}}
     print(json.dumps(out), flush=True)
 
 

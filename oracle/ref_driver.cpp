@@ -6,6 +6,7 @@
 // Used to (1) generate the golden fixtures under tests/golden/, (2) cross-check the
 // C restatement (oracle/daspmm_oracle.c), and (3) serve as bench.py's CPU reference
 // arm. Nothing in the product links it.
+#include <chrono>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -216,6 +217,28 @@ int ref_time_spmm_f32(void* hp, int kernel, int64_t P, int64_t W, int64_t C, con
         *median_s = rec.median_time;
         *min_s = rec.min_time;
         *checksum = rec.checksum;
+    });
+}
+
+// One reference spmm() call timed alone (steady_clock around exactly the user's call,
+// result dropped), on an X laid out once beforehand (as time_kernel does,
+// bench.hpp:125-137): bench.py's reference arm times one pass of its workload per step
+// this way, the same unit of work as the GPU arm's step.
+void* ref_dense_f32(const float* x, int64_t rows, int64_t cols, int colmajor) {
+    return new DenseMatrix<float>(dense_from(x, rows, cols, colmajor));
+}
+void ref_dense_free(void* d) { delete static_cast<DenseMatrix<float>*>(d); }
+int ref_time_spmm_once_f32(void* hp, void* dp, int kernel, int64_t P, int64_t W, int64_t C,
+                           double* seconds) {
+    auto* h = static_cast<RefCsr*>(hp);
+    const auto& x = *static_cast<const DenseMatrix<float>*>(dp);
+    return guarded([&] {
+        const KernelId k = KernelId::from_index(kernel);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto y = spmm(k, h->f, x, WorkerConfig{P, W, C});
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (y.data.empty() && x.num_cols > 0 && h->f.num_rows > 0) *seconds = -1.0;
     });
 }
 

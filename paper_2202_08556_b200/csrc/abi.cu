@@ -148,6 +148,7 @@ struct Knobs {
     int64_t tma_lw = 0;       // DASPMM_TMA_LW: its pairs per warp
     bool fault = false;       // SPMMKIT_ENABLE_FAULT_INJECTION=1 + DASPMM_INJECT_FAULT=1
     bool pdl = true;          // DASPMM_PDL=0: EB kernels wait for their prologue to finish
+    bool tile = true;         // DASPMM_TILE=0: no dense row-panel tile walk for RB+RM+SR
     // DASPMM_CTA_THREADS (64/128/256): CTA size of the CTA-combined EB walk. Measured:
     // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
     // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
@@ -185,6 +186,7 @@ static Knobs read_knobs() {
     k.tma_lw = i64("DASPMM_TMA_LW");
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
     k.pdl = !on("DASPMM_PDL", '0');
+    k.tile = !on("DASPMM_TILE", '0');
     if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 32 || t == 64 || t == 128 || t == 256) {
         k.cta_threads = int(t);
         k.cta_threads_set = true;
@@ -429,6 +431,22 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && !p.lean)
             p.rb_threads = kn.rb_threads;
         workers = (h->M + rpg - 1) / rpg;
+        // Row-local matrices with tiles at least half full: the dense row-panel tile walk
+        // (tile.cuh) gathers each B row once per 8-row panel instead of once per nonzero.
+        if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && h->tile_state == 1 &&
+            P <= 0 && kn.tile) {
+            p.tile = true;
+            p.lean = false;
+            p.X = 1;
+            const int64_t nvt = (std::min<int64_t>(N, 128) + p.V - 1) / p.V;  // slots per tile
+            p.L = pow2_ceil(nvt);
+            p.tile_rl = p.L <= 4 ? 8 : 1;  // narrow N: a lane per row; wide N: all 8 rows
+            const int64_t tn = int64_t(p.L) * p.V;
+            const int64_t yt = std::max<int64_t>(1, (N + tn - 1) / tn);
+            const int64_t thr = h->n_pan * p.L * p.tile_rl;
+            p.grid = dim3(unsigned((thr + 127) / 128), unsigned(yt), 1);
+            return p;
+        }
         if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact, kn.win);
         if (p.win_rows > 0) {
             p.lean = false;
@@ -478,6 +496,7 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
                    reinterpret_cast<uintptr_t>(h->coo_rows)) & 15) == 0) ? 1 : 0;
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if constexpr (std::is_same<T, float>::value) {
+        if (p.tile) return launch_rb_sr_tile(p, a, h->tile_off, h->tile_c0, h->tile_val, h->n_pan, s);
         if (p.tma) {  // prologue: split rows at warp-range ends and empty rows
             cudaError_t e = launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, 1,
                                                       static_cast<T*>(C), ldc, int(N),
@@ -533,6 +552,8 @@ int spmm_device(const daspmm_csr* h, int kernel, int64_t P, int64_t W, const voi
     // built before capture).
     if (own_scratch && (kernel >= 4 || !(kernel & 1)))
         if (int rc = ensure_coo(h, s)) return rc;
+    if (own_scratch && kernel == 0 && !exact)
+        if (int rc = ensure_tiles(h, s)) return rc;
     Plan p = plan_spmm(h, kernel, P, W, N, B, ldb, C, ldc, exact);
     if (kernel >= 4 && knobs().pdl) {
         // Programmatic launch after the EB prologue; not inside a stream capture (graph
@@ -815,10 +836,14 @@ int daspmm_csr_create_device(int64_t M, int64_t K, int64_t nnz, const int32_t* d
             daspmm_csr_destroy(h);
             return cuda_fail(e, "csr_create: cudaMalloc");
         }
-        cudaMemcpyAsync(h->rp, d_rp, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToDevice, s);
-        if (nnz > 0) {
-            cudaMemcpyAsync(h->ci, d_ci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
-            cudaMemcpyAsync(h->va, d_va, es * nnz, cudaMemcpyDeviceToDevice, s);
+        e = cudaMemcpyAsync(h->rp, d_rp, sizeof(int32_t) * (M + 1), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess && nnz > 0)
+            e = cudaMemcpyAsync(h->ci, d_ci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess && nnz > 0)
+            e = cudaMemcpyAsync(h->va, d_va, es * nnz, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) {
+            daspmm_csr_destroy(h);
+            return cuda_fail(e, "csr_create: copy");
         }
     }
     return finish_create(h, s, out);
@@ -832,9 +857,10 @@ int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1, dasp
     DeviceGuard g(full->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t ends[2] = {0, 0};
-    cudaMemcpyAsync(&ends[0], full->rp + r0, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&ends[1], full->rp + r1, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    cudaError_t e = cudaStreamSynchronize(s);
+    cudaError_t e = cudaMemcpyAsync(&ends[0], full->rp + r0, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&ends[1], full->rp + r1, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "csr_create_panel");
     const int64_t M = r1 - r0, nnz = int64_t(ends[1]) - ends[0];
     daspmm_csr* h = new daspmm_csr;
@@ -852,10 +878,15 @@ int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1, dasp
     }
     k_rebase<<<int(std::min<int64_t>((M + 256) / 256, 4096)), 256, 0, s>>>(full->rp + r0, M + 1,
                                                                           ends[0], h->rp);
-    if (nnz > 0) {
-        cudaMemcpyAsync(h->ci, full->ci + ends[0], sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
-        cudaMemcpyAsync(h->va, static_cast<const char*>(full->va) + es * ends[0], es * nnz,
-                        cudaMemcpyDeviceToDevice, s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess && nnz > 0)
+        e = cudaMemcpyAsync(h->ci, full->ci + ends[0], sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && nnz > 0)
+        e = cudaMemcpyAsync(h->va, static_cast<const char*>(full->va) + es * ends[0], es * nnz,
+                            cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) {
+        daspmm_csr_destroy(h);
+        return cuda_fail(e, "csr_create_panel: copy");
     }
     return finish_create(h, s, out);
 }
@@ -874,6 +905,9 @@ int daspmm_csr_destroy(daspmm_csr* h) {
     cudaFree(h->d_feat);
     cudaFree(h->coo_rows);
     cudaFree(h->spans);
+    cudaFree(h->tile_off);
+    cudaFree(h->tile_c0);
+    cudaFree(h->tile_val);
     delete h;
     return DASPMM_OK;
 }
@@ -1057,9 +1091,12 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
     if (kernel < 0 || kernel > 7) return fail(DASPMM_ERR_OUT_OF_RANGE, "KernelId index must be 0..7");
     DeviceGuard g(h->device);
     if (int rc = ensure_coo(h, 0)) return rc;
+    if (kernel == 0 && !(flags & DASPMM_EXACT))
+        if (int rc = ensure_tiles(h, 0)) return rc;
     const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
-    *variant = p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
-    *param = p.win_rows > 0 ? p.win_rows : (p.thr || p.tma || (p.lean && kernel >= 4)) ? p.sub
+    *variant = p.tile ? 6 : p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
+    *param = p.tile ? p.tile_rl
+             : p.win_rows > 0 ? p.win_rows : (p.thr || p.tma || (p.lean && kernel >= 4)) ? p.sub
              : p.lean ? p.rpg : int64_t(p.grid.y);
     return DASPMM_OK;
 }

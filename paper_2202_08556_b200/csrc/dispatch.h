@@ -34,6 +34,8 @@ struct Plan {
     bool repl = false;   // RB+SR with the replicated row epilogue (daspmm_spmm_rows_to)
     size_t win_smem = 0; // ... its dynamic shared memory (B window + TMA alignment lead)
     bool pdl = false;    // EB: launch the kernel programmatically after its prologue
+    bool tile = false;   // RB+RM+SR on the handle's dense row-panel tiles (tile.cuh)
+    int tile_rl = 1;     // ... row lanes per panel (1 or kTileRows); L = column lanes
 };
 
 // Kernel launch; with pdl, programmatic stream serialization: the kernel may start while
@@ -90,6 +92,9 @@ template <typename T> cudaError_t launch_rb_sr(const Plan&, const SpmmArgs<T>&, 
 template <typename T> cudaError_t launch_rb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_sr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, cudaStream_t);
+// RB+RM+SR on dense row-panel tiles (spmm_tile.cu); p.L column lanes x p.tile_rl rows.
+cudaError_t launch_rb_sr_tile(const Plan&, const SpmmArgs<float>&, const int* off, const int* c0,
+                              const float* val, int64_t n_pan, cudaStream_t);
 // PR groups wider than a warp (W = 64 .. 1024), RB and EB (spmm_pr_wide.cu).
 template <typename T> cudaError_t launch_pr_wide(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T>

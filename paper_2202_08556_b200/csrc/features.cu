@@ -11,6 +11,7 @@
 // sequential replay kernel below, which reproduces the reference bits.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -119,6 +120,133 @@ int ensure_coo(const daspmm_csr* hc, cudaStream_t s) {
     return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "coo_rows");
 }
 
+// ---------------------------------------------------------------- dense row-panel tiles
+// One warp per 8-row panel (tile.cuh): the panel's column window [lo, hi] and whether
+// every row lists its columns in strictly ascending order (the tile walk adds a row's
+// products in column order, which is the CSR order only then).
+constexpr int kPanelRows = 8;
+
+__global__ void k_tile_spans(const int* __restrict__ rp, const int* __restrict__ ci, int M,
+                             int64_t n_pan, int* __restrict__ width, int* __restrict__ c0,
+                             int* __restrict__ unsorted) {
+    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n_pan) return;
+    const int r0 = int(p * kPanelRows), r1 = min(M, r0 + kPanelRows);
+    int lo = INT_MAX, hi = -1;
+    bool bad = false;
+    for (int r = r0; r < r1; ++r) {
+        const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+        for (int i = s + lane; i < e; i += 32) {
+            const int c = __ldg(ci + i);
+            lo = min(lo, c);
+            hi = max(hi, c);
+            if (i + 1 < e && __ldg(ci + i + 1) <= c) bad = true;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *unsorted = 1;
+    if (lane == 0) {
+        width[p] = hi >= lo ? hi - lo + 1 : 0;
+        c0[p] = hi >= lo ? lo : 0;
+    }
+}
+
+// One warp per panel: zero its tile, then place every nonzero at (col - c0, row - r0).
+__global__ void k_tile_fill(const int* __restrict__ rp, const int* __restrict__ ci,
+                            const float* __restrict__ va, int M, int64_t n_pan,
+                            const int* __restrict__ off, const int* __restrict__ c0,
+                            float* __restrict__ val) {
+    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n_pan) return;
+    const int o0 = off[p], o1 = off[p + 1], base = c0[p];
+    for (int i = o0 + lane; i < o1; i += 32) val[i] = 0.f;
+    __syncwarp();
+    const int r0 = int(p * kPanelRows), r1 = min(M, r0 + kPanelRows);
+    for (int r = r0; r < r1; ++r) {
+        const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+        for (int i = s + lane; i < e; i += 32)
+            val[o0 + (__ldg(ci + i) - base) * kPanelRows + (r - r0)] = __ldg(va + i);
+    }
+}
+
+// Builds the tiles once per handle when they pay: fp32, rows column-sorted, and at least
+// DASPMM_TILE_FILL (default 0.5) of the tile cells holding a nonzero — then each staged
+// B row serves >= 4 nonzeros and the tiles take no more bytes than CSR's (col, val).
+int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
+    daspmm_csr* h = const_cast<daspmm_csr*>(hc);
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->tile_state != 0) return DASPMM_OK;
+    h->tile_state = -1;
+    if (h->dtype != DASPMM_F32 || h->M <= 0 || h->nnz <= 0) return DASPMM_OK;
+    static const double min_fill = [] {
+        const char* e = getenv("DASPMM_TILE_FILL");
+        return e ? atof(e) : 0.5;
+    }();
+    if (min_fill > 1.0) return DASPMM_OK;  // DASPMM_TILE_FILL=2 turns the variant off
+    const int64_t n_pan = (h->M + kPanelRows - 1) / kPanelRows;
+    int *d_w = nullptr, *d_bad = nullptr;
+    cudaError_t e = cudaMalloc(&d_w, sizeof(int) * size_t(n_pan));
+    if (e == cudaSuccess) e = cudaMalloc(&h->tile_c0, sizeof(int) * size_t(n_pan));
+    if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, sizeof(int), s);
+    if (e == cudaSuccess) {
+        const int64_t threads = n_pan * 32;
+        k_tile_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M), n_pan,
+                                                                    d_w, h->tile_c0, d_bad);
+        e = cudaGetLastError();
+    }
+    std::vector<int> w(size_t(n_pan), 0);
+    int bad = 1;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(w.data(), d_w, sizeof(int) * w.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d_w);
+    cudaFree(d_bad);
+    auto give_up = [&](cudaError_t err) {
+        cudaFree(h->tile_c0);
+        h->tile_c0 = nullptr;
+        return err == cudaSuccess ? DASPMM_OK : cuda_fail(err, "tiles");
+    };
+    if (e != cudaSuccess) return give_up(e);
+    std::vector<int> off(size_t(n_pan) + 1, 0);
+    int64_t total = 0;
+    for (int64_t p = 0; p < n_pan; ++p) {
+        off[size_t(p)] = int(total);
+        total += int64_t(w[size_t(p)]) * kPanelRows;
+        if (total >= (int64_t(1) << 31) - 64) return give_up(cudaSuccess);
+    }
+    off[size_t(n_pan)] = int(total);
+    h->tile_fill = total > 0 ? double(h->nnz) / double(total) : 0.0;
+    if (bad || h->tile_fill < min_fill) return give_up(cudaSuccess);
+    if ((e = cudaMalloc(&h->tile_off, sizeof(int) * off.size())) != cudaSuccess ||
+        (e = cudaMalloc(&h->tile_val, sizeof(float) * size_t(std::max<int64_t>(total, 8)))) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(h->tile_off, off.data(), sizeof(int) * off.size(),
+                             cudaMemcpyHostToDevice, s)) != cudaSuccess) {
+        cudaFree(h->tile_off);
+        cudaFree(h->tile_val);
+        h->tile_off = nullptr;
+        h->tile_val = nullptr;
+        cudaGetLastError();
+        return give_up(cudaSuccess);  // no room: the base walk serves the call
+    }
+    const int64_t threads = n_pan * 32;
+    k_tile_fill<<<unsigned((threads + 255) / 256), 256, 0, s>>>(
+        h->rp, h->ci, static_cast<const float*>(h->va), int(h->M), n_pan, h->tile_off, h->tile_c0,
+        h->tile_val);
+    if ((e = cudaGetLastError()) == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "tiles: fill");
+    h->n_pan = n_pan;
+    h->tile_state = 1;
+    return DASPMM_OK;
+}
+
 // Column window of every 32-row fine panel: one warp per panel, [min, max] column
 // ({INT_MAX, -1} when the panel holds no nonzero).
 __global__ void k_fine_spans(const int* __restrict__ rp, const int* __restrict__ ci, int M,
@@ -152,8 +280,10 @@ static int compute_spans(daspmm_csr* h, cudaStream_t s) {
     k_fine_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M),
                                                                  h->n_fine, h->spans);
     std::vector<int2> hs(size_t(h->n_fine));
-    cudaMemcpyAsync(hs.data(), h->spans, sizeof(int2) * hs.size(), cudaMemcpyDeviceToHost, s);
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "spans");
+    if ((e = cudaGetLastError()) == cudaSuccess)
+        e = cudaMemcpyAsync(hs.data(), h->spans, sizeof(int2) * hs.size(), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "spans");
     for (int i = 0; i < daspmm_csr::kSpanLevels; ++i) {
         const int64_t k = int64_t(1) << i;
         int64_t mx = 0, cnt = 0;
@@ -200,8 +330,10 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
         return cuda_fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&bitmap, sizeof(unsigned) * std::max<int64_t>(words, 1))) != cudaSuccess)
         return cuda_fail(e, "cudaMalloc");
-    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s);
-    cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max<int64_t>(words, 1), s);
+    if ((e = cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(bitmap, 0, sizeof(unsigned) * std::max<int64_t>(words, 1), s)) !=
+            cudaSuccess)
+        return cuda_fail(e, "features: memset");
     if (M > 0)
         k_row_terms<<<blocks, kFeatThreads, 0, s>>>(h->rp, M, f.mean, partial, h->empty_rows,
                                                      counters);
@@ -213,8 +345,12 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
     }
     std::vector<double> hp(blocks, 0.0);
     unsigned long long hc[2] = {0, 0};
-    if (M > 0) cudaMemcpyAsync(hp.data(), partial, sizeof(double) * blocks, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "features: launch");
+    if (M > 0 && (e = cudaMemcpyAsync(hp.data(), partial, sizeof(double) * blocks,
+                                      cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "features: copy");
+    if ((e = cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e, "features: copy");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "features");
     trace_mark("features: kernels+sync");
     cudaFree(partial);

@@ -161,6 +161,8 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     if ((e = cudaEventCreateWithFlags(&en.done, cudaEventDisableTiming)) != cudaSuccess)
         return cuda_fail(e, "graph: event");
     if (int rc = ensure_coo(h, 0)) return rc;  // EB bodies read COO row ids
+    if (!(k.flags & DASPMM_EXACT))
+        if (int rc = ensure_tiles(h, 0)) return rc;  // RB+RM+SR body may walk the tiles
     // Scratch: EB chunk rows for the largest plan, and B in the other layout.
     int64_t max_p = 1;
     for (int kid = 4; kid < 8; ++kid) {

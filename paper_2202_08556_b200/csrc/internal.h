@@ -68,6 +68,15 @@ struct daspmm_csr {
     static constexpr int kSpanLevels = 8;
     int64_t span_max[kSpanLevels] = {};
     double span_avg[kSpanLevels] = {};
+    // Dense row-panel tiles of 8 rows (tile.cuh), fp32 only, built on the first fast
+    // RB+RM+SR call (ensure_tiles) when rows are column-sorted and the tiles are at least
+    // half full: tile_off[n_pan + 1] (floats), tile_c0[n_pan], tile_val (k-major tiles).
+    int tile_state = 0;  // 0 not examined, 1 built, -1 not worth it
+    int64_t n_pan = 0;
+    double tile_fill = 0.0;
+    int32_t* tile_off = nullptr;
+    int32_t* tile_c0 = nullptr;
+    float* tile_val = nullptr;
     // Row-panel handles built by daspmm_multi_spmm (one per (parts, rank)), destroyed
     // with this handle (multi.cu).
     struct PanelEntry {
@@ -83,6 +92,8 @@ int compute_features(daspmm_csr* h, cudaStream_t s);
 // Builds h->coo_rows once (never call inside a stream capture).
 int ensure_coo(const daspmm_csr* h, cudaStream_t s);
 int exact_std(daspmm_csr* h, double* out);
+// Examines / builds h's dense row-panel tiles once (never call inside a stream capture).
+int ensure_tiles(const daspmm_csr* h, cudaStream_t s);
 // Implemented in abi.cu
 struct Plan;
 // base_only: the design point's base kernel (no lean / window / TMA launch variants).

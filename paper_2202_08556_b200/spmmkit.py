@@ -443,7 +443,8 @@ def reload_env():
     check(lib().daspmm_reload_env())
 
 
-PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma"}
+PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma",
+                 6: "rb_tile"}
 
 
 def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False):
