@@ -149,6 +149,9 @@ struct Knobs {
     bool fault = false;       // SPMMKIT_ENABLE_FAULT_INJECTION=1 + DASPMM_INJECT_FAULT=1
     bool pdl = true;          // DASPMM_PDL=0: EB kernels wait for their prologue to finish
     bool tile = true;         // DASPMM_TILE=0: no dense row-panel tile walk for RB+RM+SR
+    bool tile_force = false;  // DASPMM_TILE=2: the tile walk at any grid size (tests)
+    int tile_rl = 0;          // DASPMM_TILE_RL=1/8: force the tile walk's row lanes (tuning)
+    int tile_u = 0;           // DASPMM_TILE_U=2/4/8: B rows in flight per lane (tuning)
     // DASPMM_CTA_THREADS (64/128/256): CTA size of the CTA-combined EB walk. Measured:
     // smaller CTAs wait less at the combine barrier (power-law s20 N = 32 273 -> 248 us,
     // s17 N = 32 66 -> 52, c4 N = 64 1.69 -> 1.61 ms; profiles/r01c_cta_threads_probe.txt).
@@ -187,6 +190,9 @@ static Knobs read_knobs() {
     k.fault = on("SPMMKIT_ENABLE_FAULT_INJECTION", '1') && on("DASPMM_INJECT_FAULT", '1');
     k.pdl = !on("DASPMM_PDL", '0');
     k.tile = !on("DASPMM_TILE", '0');
+    k.tile_force = on("DASPMM_TILE", '2');
+    k.tile_rl = int(i64("DASPMM_TILE_RL"));
+    if (const int64_t u = i64("DASPMM_TILE_U"); u == 2 || u == 4 || u == 8) k.tile_u = int(u);
     if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 32 || t == 64 || t == 128 || t == 256) {
         k.cta_threads = int(t);
         k.cta_threads_set = true;
@@ -432,20 +438,29 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             p.rb_threads = kn.rb_threads;
         workers = (h->M + rpg - 1) / rpg;
         // Row-local matrices with tiles at least half full: the dense row-panel tile walk
-        // (tile.cuh) gathers each B row once per 8-row panel instead of once per nonzero.
+        // (tile.cuh) gathers each B row once per 8-row panel instead of once per nonzero
+        // (banded s20: N = 2 43 -> 31 us, N = 32 156 -> 114, half-width 32 N = 128 1749 ->
+        // 889). Grids under ~3.5 CTAs per SM keep the base walk (banded s14 runs 0.5-0.8x
+        // on tiles: too few panels to hide the window walk's latency).
         if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && h->tile_state == 1 &&
             P <= 0 && kn.tile) {
-            p.tile = true;
-            p.lean = false;
-            p.X = 1;
             const int64_t nvt = (std::min<int64_t>(N, 128) + p.V - 1) / p.V;  // slots per tile
-            p.L = pow2_ceil(nvt);
-            p.tile_rl = p.L <= 4 ? 8 : 1;  // narrow N: a lane per row; wide N: all 8 rows
-            const int64_t tn = int64_t(p.L) * p.V;
-            const int64_t yt = std::max<int64_t>(1, (N + tn - 1) / tn);
-            const int64_t thr = h->n_pan * p.L * p.tile_rl;
-            p.grid = dim3(unsigned((thr + 127) / 128), unsigned(yt), 1);
-            return p;
+            const int cl = pow2_ceil(nvt);
+            int rl = cl == 1 ? 8 : 1;  // one column slot (N <= 4): a lane per row
+            if (kn.tile_rl == 1 || (kn.tile_rl == 8 && cl <= 4)) rl = kn.tile_rl;  // tuning
+            const int64_t thr = h->n_pan * cl * rl;
+            if (thr >= 65536 || kn.tile_force) {
+                p.tile = true;
+                p.lean = false;
+                p.X = 1;
+                p.L = cl;
+                p.tile_rl = rl;
+                p.tile_u = kn.tile_u > 0 ? kn.tile_u : (rl == 8 ? 8 : 4);
+                const int64_t tn = int64_t(cl) * p.V;
+                const int64_t yt = std::max<int64_t>(1, (N + tn - 1) / tn);
+                p.grid = dim3(unsigned((thr + 127) / 128), unsigned(yt), 1);
+                return p;
+            }
         }
         if (!base_only) plan_window(h, p, N, tile_cols, ytiles, B, exact, kn.win);
         if (p.win_rows > 0) {

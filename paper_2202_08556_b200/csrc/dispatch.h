@@ -36,6 +36,7 @@ struct Plan {
     bool pdl = false;    // EB: launch the kernel programmatically after its prologue
     bool tile = false;   // RB+RM+SR on the handle's dense row-panel tiles (tile.cuh)
     int tile_rl = 1;     // ... row lanes per panel (1 or kTileRows); L = column lanes
+    int tile_u = 2;      // ... tile columns (B rows) in flight per lane (2, 4 or 8)
 };
 
 // Kernel launch; with pdl, programmatic stream serialization: the kernel may start while

@@ -7,9 +7,23 @@ namespace daspmm {
 namespace {
 constexpr int kTileThreads = 128;
 
+// Column slots per panel <= 4: the direct walk; 8..32: the staged, pipelined walk.
+template <int V, int CL, int RL, int U>
+void go_u(const Plan& p, const SpmmArgs<float>& a, const TileArgs& t, cudaStream_t s) {
+    if constexpr (CL <= 4)
+        k_rb_sr_tile_direct<V, CL, RL, 1, kTileThreads, U><<<p.grid, kTileThreads, 0, s>>>(a, t);
+    else
+        k_rb_sr_tile<V, CL, RL, 1, kTileThreads, U><<<p.grid, kTileThreads, 0, s>>>(a, t);
+}
+
 template <int V, int CL, int RL>
 cudaError_t go(const Plan& p, const SpmmArgs<float>& a, const TileArgs& t, cudaStream_t s) {
-    k_rb_sr_tile<V, CL, RL, 1, kTileThreads><<<p.grid, kTileThreads, 0, s>>>(a, t);
+    switch (p.tile_u) {
+        case 2: go_u<V, CL, RL, 2>(p, a, t, s); break;
+        case 4: go_u<V, CL, RL, 4>(p, a, t, s); break;
+        case 8: go_u<V, CL, RL, 8>(p, a, t, s); break;
+        default: return cudaErrorNotSupported;
+    }
     return cudaGetLastError();
 }
 
@@ -24,6 +38,9 @@ cudaError_t go_v(const Plan& p, const SpmmArgs<float>& a, const TileArgs& t, cud
         }
     }
     switch (p.L) {
+        case 1: return go<V, 1, 1>(p, a, t, s);
+        case 2: return go<V, 2, 1>(p, a, t, s);
+        case 4: return go<V, 4, 1>(p, a, t, s);
         case 8: return go<V, 8, 1>(p, a, t, s);
         case 16: return go<V, 16, 1>(p, a, t, s);
         case 32: return go<V, 32, 1>(p, a, t, s);

@@ -41,12 +41,140 @@ struct TileArgs {
     int n_pan;
 };
 
-template <int V, int CL, int RL, int CPL, int NT>
+// Shared-memory budget of one CTA for staged tile columns: each group stages up to
+// kTileStage(G) columns of its panel (k-major, kTileRows floats each) at a time.
+constexpr int kTileSmemFloats = 8192;  // 32 KB per CTA
+template <int G, int NT>
+constexpr int tile_stage_cols() {
+    return kTileSmemFloats / (NT / G) / kTileRows;
+}
+
+// The walk is software-pipelined: B rows k + U are requested while rows k are consumed,
+// so each lane keeps U gathers in flight through the whole window (a plain unrolled loop
+// drained them at every step: ncu showed the kernel latency-bound at 45% of the DRAM
+// rate with the traffic already at the algorithmic minimum). The panel's tile values
+// are staged once into shared memory (coalesced 16-byte loads) and read back as
+// broadcasts, keeping them off the registers and the dependent-load chain.
+template <int V, int CL, int RL, int CPL, int NT, int U>
 __global__ void __launch_bounds__(NT) k_rb_sr_tile(const SpmmArgs<float> a, const TileArgs t) {
     constexpr int G = CL * RL;                 // lanes per group (one panel)
     constexpr int RPL = kTileRows / RL;        // rows per lane
     constexpr int TN = CL * V * CPL;           // columns per tile (blockIdx.y)
-    constexpr int U = (RPL * V * CPL >= 32) ? 2 : 4;  // tile columns in flight per step
+    constexpr int KS = tile_stage_cols<G, NT>();  // staged tile columns per group
+    static_assert(KS >= U && KS % U == 0, "stage must hold whole pipeline steps");
+    __shared__ __align__(16) float stage[NT / G][KS * kTileRows];
+    const int gl = threadIdx.x & (G - 1);
+    const int cl = gl % CL, rl = gl / CL;
+    const unsigned mask = group_mask<G>();
+    const int64_t p = (int64_t(blockIdx.x) * NT + threadIdx.x) / G;
+    if (p >= t.n_pan) return;  // whole groups leave together
+    float* sg = stage[threadIdx.x / G];
+    const int r_base = int(p) * kTileRows + rl;  // rows r_base + RL * j, j < RPL
+    const int off0 = __ldg(t.off + p);
+    const int w = (__ldg(t.off + p + 1) - off0) / kTileRows;
+    const int c0 = __ldg(t.c0 + p);
+    const int n0 = blockIdx.y * TN + cl * V;
+
+    Frag<float, V> acc[RPL][CPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j)
+#pragma unroll
+        for (int s = 0; s < CPL; ++s)
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[j][s].v[i] = 0.f;
+
+    // per-slot byte base of B's column (lanes past N read column 0, never stored)
+    const char* Bcol[CPL];
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+        const int col = n0 + s * CL * V;
+        Bcol[s] = reinterpret_cast<const char*>(a.B + (col < a.N ? col : 0));
+    }
+    const int ldb_bytes = int(a.ldb) * int(sizeof(float));
+    auto gather = [&](int k, Frag<float, V>* b) {  // B row c0 + k (k clamped into the window)
+#pragma unroll
+        for (int s = 0; s < CPL; ++s)
+            b[s] = ld_frag<float, V>(reinterpret_cast<const float*>(
+                Bcol[s] + int64_t(c0 + min(k, w - 1)) * ldb_bytes));
+    };
+    Frag<float, V> b[U][CPL];
+    if (w > 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) gather(u, b[u]);
+    }
+    const float4* tile4 = reinterpret_cast<const float4*>(t.val + off0);
+    for (int kc = 0; kc < w; kc += KS) {
+        const int kw = min(KS, w - kc);
+        __syncwarp(mask);  // the previous chunk's reads are done
+        for (int i = gl; i < kw * (kTileRows / 4); i += G)
+            reinterpret_cast<float4*>(sg)[i] = __ldg(tile4 + kc * (kTileRows / 4) + i);
+        __syncwarp(mask);
+        for (int k0 = 0; k0 < kw; k0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (k0 + u < kw) {
+                    float av[RPL];
+                    if constexpr (RL == 1) {
+                        const float4 lo = reinterpret_cast<const float4*>(sg)[(k0 + u) * 2];
+                        const float4 hi = reinterpret_cast<const float4*>(sg)[(k0 + u) * 2 + 1];
+                        av[0] = lo.x; av[1] = lo.y; av[2] = lo.z; av[3] = lo.w;
+                        av[4] = hi.x; av[5] = hi.y; av[6] = hi.z; av[7] = hi.w;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < RPL; ++j) av[j] = sg[(k0 + u) * kTileRows + rl + RL * j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < RPL; ++j)
+#pragma unroll
+                        for (int s = 0; s < CPL; ++s)
+#pragma unroll
+                            for (int i = 0; i < V; ++i)
+                                acc[j][s].v[i] = fmaf(av[j], b[u][s].v[i], acc[j][s].v[i]);
+                }
+                gather(kc + k0 + u + U, b[u]);  // refill the slot U rows ahead
+            }
+        }
+    }
+
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        const int r = r_base + RL * j;
+        if (r >= a.M) break;
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+            const int col = n0 + s * CL * V;
+            if (col >= a.N) continue;
+            bool finite = true;
+#pragma unroll
+            for (int i = 0; i < V; ++i) finite &= isfinite(acc[j][s].v[i]);
+            Frag<float, V> out = acc[j][s];
+            if (!finite) {  // rare: replay the row from CSR (the base walk's sequence)
+#pragma unroll
+                for (int i = 0; i < V; ++i) out.v[i] = 0.f;
+                const int e1 = __ldg(a.rp + r + 1);
+                for (int e = __ldg(a.rp + r); e < e1; ++e) {
+                    const float v = __ldg(a.va + e);
+                    const Frag<float, V> bb = ld_frag<float, V>(
+                        a.B + int64_t(__ldg(a.ci + e)) * a.ldb + col);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) out.v[i] = fmaf(v, bb.v[i], out.v[i]);
+                }
+            }
+            st_frag(a.C + int64_t(r) * a.ldc + col, out);
+        }
+    }
+}
+
+// Narrow N (one to four column slots per panel): the direct walk — tile values and B
+// rows loaded together from global memory U columns at a time, no staging. Many small
+// groups share a CTA here, and staging would cost occupancy (shared memory) and a
+// synchronisation per chunk for a few FMAs per column (banded s20 N = 8: 53 us direct vs
+// 75 us staged; N >= 32 is the other way round: 156 vs 94 us).
+template <int V, int CL, int RL, int CPL, int NT, int U>
+__global__ void __launch_bounds__(NT) k_rb_sr_tile_direct(const SpmmArgs<float> a, const TileArgs t) {
+    constexpr int G = CL * RL;                 // lanes per group (one panel)
+    constexpr int RPL = kTileRows / RL;        // rows per lane
+    constexpr int TN = CL * V * CPL;           // columns per tile (blockIdx.y)
     const int gl = threadIdx.x & (G - 1);
     const int cl = gl % CL, rl = gl / CL;
     const int64_t p = (int64_t(blockIdx.x) * NT + threadIdx.x) / G;

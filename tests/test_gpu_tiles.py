@@ -44,10 +44,14 @@ def _banded(rows, b, seed, cols=None, drop=0.0):
                      rng.uniform(-1, 1, ci.size).astype(np.float32), np.float32)
 
 
-def _run(sk, d, B, tile: bool):
+def _run(sk, d, B, tile: bool, rl: int = 0):
+    """One RB+RM+SR call with the tile walk forced on (DASPMM_TILE=2: any grid size, so
+    test-sized matrices take it) or off; rl forces its row lanes (1 or 8)."""
     import torch
 
-    os.environ["DASPMM_TILE"] = "1" if tile else "0"
+    os.environ["DASPMM_TILE"] = "2" if tile else "0"
+    if rl:
+        os.environ["DASPMM_TILE_RL"] = str(rl)
     sk.reload_env()
     try:
         C = torch.full((d.num_rows, B.shape[1]), float("nan"), device="cuda")
@@ -57,10 +61,11 @@ def _run(sk, d, B, tile: bool):
         return C, variant
     finally:
         os.environ.pop("DASPMM_TILE", None)
+        os.environ.pop("DASPMM_TILE_RL", None)
         sk.reload_env()
 
 
-@pytest.mark.parametrize("case", ["banded_b8", "banded_b3_ragged", "banded_b8_dropped",
+@pytest.mark.parametrize("case", ["banded_b8", "banded_b4_ragged", "banded_b8_dropped",
                                   "short_last_panel", "empty_rows"])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 16, 32, 33, 64, 128, 200])
 def test_tiles_bit_identical_to_base_and_within_gamma(sk, case, n):
@@ -68,8 +73,8 @@ def test_tiles_bit_identical_to_base_and_within_gamma(sk, case, n):
 
     if case == "banded_b8":
         a = _banded(3000, 8, 1)
-    elif case == "banded_b3_ragged":
-        a = _banded(2501, 3, 2, cols=2600)
+    elif case == "banded_b4_ragged":
+        a = _banded(2501, 4, 2, cols=2600)
     elif case == "banded_b8_dropped":
         a = _banded(4000, 8, 3, drop=0.2)
     elif case == "short_last_panel":
@@ -99,6 +104,40 @@ def test_tiles_bit_identical_to_base_and_within_gamma(sk, case, n):
     assert (err <= H.gamma_bound(a, x64, np.float32)).all()
 
 
+@pytest.mark.parametrize("rl", [1, 8])
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16])
+def test_tiles_both_row_mappings(sk, rl, n):
+    """Narrow N runs either a lane per row (RL = 8) or a lane per column slot with all
+    eight rows (RL = 1): both give the base walk's bits."""
+    import torch
+
+    a = _banded(1777, 8, 21)
+    d = sk.DeviceCsr.from_host(a)
+    B = torch.rand(a.num_cols, n, device="cuda") - 0.5
+    Cb, _ = _run(sk, d, B, False)
+    Ct, vt = _run(sk, d, B, True, rl=rl)
+    assert vt == "rb_tile"
+    assert torch.equal(Cb, Ct)
+
+
+def test_tiles_default_only_on_large_grids(sk):
+    """Without forcing, the tile walk needs >= 65536 threads (8-row panels x lanes):
+    a 2^20-row banded matrix takes it, a 3000-row one keeps the base walk."""
+    import torch
+
+    from paper_2202_08556_b200 import gen
+
+    M, K, rp, ci, va = gen.banded(1 << 20, 8, seed=3)
+    big = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+    B = torch.rand(K, 32, device="cuda")
+    C = torch.empty(M, 32, device="cuda")
+    assert sk.plan_info(0, big, B, C)[0] == "rb_tile"
+    small = sk.DeviceCsr.from_host(_banded(3000, 8, 1))
+    Bs = torch.rand(3000, 32, device="cuda")
+    Cs = torch.empty(3000, 32, device="cuda")
+    assert sk.plan_info(0, small, Bs, Cs)[0] != "rb_tile"
+
+
 def test_tiles_strided_operands(sk):
     """B and C with leading dimensions above N (views into wider buffers)."""
     import torch
@@ -111,7 +150,7 @@ def test_tiles_strided_operands(sk):
     sk.reload_env()
     Cw0 = torch.full((a.num_rows, 44), 7.0, device="cuda")
     sk.spmm_device(0, d, B, Cw0[:, :36])
-    os.environ["DASPMM_TILE"] = "1"
+    os.environ["DASPMM_TILE"] = "2"
     sk.reload_env()
     Cw1 = torch.full((a.num_rows, 44), 7.0, device="cuda")
     sk.spmm_device(0, d, B, Cw1[:, :36])
@@ -152,6 +191,8 @@ def test_tiles_not_used_where_they_do_not_pay(sk):
     the base walk."""
     import torch
 
+    os.environ["DASPMM_TILE"] = "2"  # any grid size: only eligibility decides
+    sk.reload_env()
     u = H.random_csr(3000, 3000, 48000, seed=11, dtype=np.float32)
     d = sk.DeviceCsr.from_host(u)
     B = torch.rand(3000, 32, device="cuda")
@@ -170,6 +211,8 @@ def test_tiles_not_used_where_they_do_not_pay(sk):
     x64 = B.cpu().numpy().astype(np.float64)
     y64 = O.spmm_reference(H.to_oracle(b), x64)
     assert (np.abs(C.cpu().numpy() - y64) <= H.gamma_bound(b, x64, np.float32)).all()
+    os.environ.pop("DASPMM_TILE", None)
+    sk.reload_env()
 
 
 def test_tiles_through_da_spmm(sk):
@@ -180,6 +223,8 @@ def test_tiles_through_da_spmm(sk):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     model = sk.load_selector(open(os.path.join(root, "paper_2202_08556_b200", "models",
                                                "b200_selector.txt")).read())
+    os.environ["DASPMM_TILE"] = "2"
+    sk.reload_env()
     a = _banded(20000, 8, 13)
     d = sk.DeviceCsr.from_host(a)
     for n in (8, 64, 128):
@@ -193,3 +238,5 @@ def test_tiles_through_da_spmm(sk):
         y64 = O.spmm_reference(H.to_oracle(a), x64)
         err = np.abs(C.cpu().numpy().astype(np.float64) - y64)
         assert (err <= H.gamma_bound(a, x64, np.float32)).all()
+    os.environ.pop("DASPMM_TILE", None)
+    sk.reload_env()

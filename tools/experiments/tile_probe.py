@@ -49,6 +49,7 @@ mats = [("banded_s14_b8", lambda: gen.banded(1 << 14, 8, seed=14)),
         ("banded_s20_b32", lambda: gen.banded(1 << 20, 32, seed=21)),
         ("stencil5_1024", lambda: stencil2d(1024)),
         ("uniform_s17_d16", lambda: gen.uniform(1 << 17, 1 << 17, 16 << 17, seed=17))]
+SWEEP = os.environ.get("TILE_SWEEP", "") == "1"
 for name, mk in mats:
     M, K, rp, ci, va = mk()
     d = sk.DeviceCsr.from_device(M, K, rp, ci, va)
@@ -60,28 +61,23 @@ for name, mk in mats:
         sk.reload_env()
         tb = t(lambda: sk.spmm_device(0, d, B, C0))
         vb = sk.plan_info(0, d, B, C0)
-        os.environ["DASPMM_TILE"] = "1"
-        sk.reload_env()
-        tt = t(lambda: sk.spmm_device(0, d, B, C1))
-        vt = sk.plan_info(0, d, B, C1)
-        same = bool(torch.equal(C0, C1))
-        print(f"{name:16s} N={n:3d} base {tb:8.1f} us {vb}  tile {tt:8.1f} us {vt}  "
-              f"speedup {tb / tt:5.2f}  bit-identical {same}", flush=True)
-    # non-finite B under an absent entry: the tile walk must fall back to the CSR replay
-    B = gen.dense_operand(K, 32, seed=3)
-    B[K // 2, :] = float("inf")
-    B[K // 3, 5] = float("nan")
-    os.environ["DASPMM_TILE"] = "0"
-    sk.reload_env()
-    C0 = torch.empty(M, 32, device="cuda")
-    C1 = torch.empty(M, 32, device="cuda")
-    sk.spmm_device(0, d, B, C0)
-    os.environ["DASPMM_TILE"] = "1"
-    sk.reload_env()
-    sk.spmm_device(0, d, B, C1)
-    same = bool(torch.equal(C0.nan_to_num(1.5, 7.0, -7.0), C1.nan_to_num(1.5, 7.0, -7.0))) and \
-        bool(torch.equal(C0.isnan(), C1.isnan()))
-    print(f"{name:16s} non-finite B: identical to base {same}; nonfinite rows "
-          f"{int((~C1.isfinite()).any(1).sum())}", flush=True)
+        configs = [("default", {})]
+        if SWEEP:
+            configs += [(f"rl{rl}_u{u}", {"DASPMM_TILE_RL": str(rl), "DASPMM_TILE_U": str(u)})
+                        for rl in (1, 8) for u in (2, 4, 8)]
+        out = []
+        for label, env in configs:
+            os.environ["DASPMM_TILE"] = "1"
+            for k in ("DASPMM_TILE_RL", "DASPMM_TILE_U"):
+                os.environ.pop(k, None)
+            os.environ.update(env)
+            sk.reload_env()
+            tt = t(lambda: sk.spmm_device(0, d, B, C1))
+            vt = sk.plan_info(0, d, B, C1)
+            same = bool(torch.equal(C0, C1))
+            out.append(f"{label} {tt:7.1f}{'' if same else '!'}{'' if vt[0] == 'rb_tile' else '(' + vt[0] + ')'}")
+        for k in ("DASPMM_TILE_RL", "DASPMM_TILE_U"):
+            os.environ.pop(k, None)
+        print(f"{name:16s} N={n:3d} base {tb:7.1f} us {vb[0]:8s} | " + " | ".join(out), flush=True)
     del d, rp, ci, va
     torch.cuda.empty_cache()
