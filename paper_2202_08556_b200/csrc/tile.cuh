@@ -55,8 +55,11 @@ constexpr int tile_stage_cols() {
 // rate with the traffic already at the algorithmic minimum). The panel's tile values
 // are staged once into shared memory (coalesced 16-byte loads) and read back as
 // broadcasts, keeping them off the registers and the dependent-load chain.
+#ifndef DASPMM_TILE_MINB
+#define DASPMM_TILE_MINB 1
+#endif
 template <int V, int CL, int RL, int CPL, int NT, int U>
-__global__ void __launch_bounds__(NT) k_rb_sr_tile(const SpmmArgs<float> a, const TileArgs t) {
+__global__ void __launch_bounds__(NT, DASPMM_TILE_MINB) k_rb_sr_tile(const SpmmArgs<float> a, const TileArgs t) {
     constexpr int G = CL * RL;                 // lanes per group (one panel)
     constexpr int RPL = kTileRows / RL;        // rows per lane
     constexpr int TN = CL * V * CPL;           // columns per tile (blockIdx.y)

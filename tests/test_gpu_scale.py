@@ -106,7 +106,11 @@ VARIANTS = [
     ("suite", "powerlaw_s20_d16", 64, 4, {"DASPMM_TMA": "1"}, "eb_tma"),
     ("suite", "powerlaw_s20_d16", 8, 5, {}, "base"),            # EB+PR, conditional scan
     ("suite", "uniform_s20_d16", 8, 1, {}, "base"),             # RB+PR, tree
-    ("suite", "banded_s20_b8", 128, 0, {"DASPMM_WIN": "1"}, "rb_window"),
+    ("suite", "banded_s20_b8", 128, 0, {"DASPMM_WIN": "1", "DASPMM_TILE": "0"}, "rb_window"),
+    ("suite", "banded_s20_b8", 128, 0, {}, "rb_tile"),          # staged, pipelined walk
+    ("suite", "banded_s20_b8", 16, 0, {}, "rb_tile"),           # direct walk, lane per slot
+    ("suite", "banded_s20_b8", 2, 0, {}, "rb_tile"),            # direct walk, lane per row
+    ("suite", "banded_s20_b8", 33, 0, {}, "rb_tile"),           # V = 1, two column tiles
     ("suite", "banded_s20_b8", 2, 4, {}, "eb_thread"),
     ("suite", "uniform_s17_d16", 8, 2, {}, "base"),             # CM kernels (col-major B)
     ("suite", "uniform_s17_d16", 8, 3, {}, "base"),

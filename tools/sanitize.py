@@ -68,6 +68,21 @@ for n in (2, 8, 32, 128):
     sk.spmm_device(0, d, B, C)
 del os.environ["DASPMM_WIN"]
 sk.reload_env()
+# dense row-panel tile walks (forced at this size): direct (N <= 16) and staged (N >= 32),
+# both row mappings, a non-finite B row (CSR replay path), strided B
+os.environ["DASPMM_TILE"] = "2"
+for rl in ("1", "8"):
+    os.environ["DASPMM_TILE_RL"] = rl
+    sk.reload_env()
+    for n in (1, 2, 4, 8, 16, 33, 64, 128, 200):
+        B = torch.rand(2000, n, device="cuda")
+        B[777, 0] = float("inf")
+        C = torch.empty(2000, n, device="cuda")
+        sk.spmm_device(0, d, B, C)
+    Bw = torch.rand(2000, 40, device="cuda")[:, :36]
+    sk.spmm_device(0, d, Bw, torch.empty(2000, 36, device="cuda"))
+del os.environ["DASPMM_TILE"], os.environ["DASPMM_TILE_RL"]
+sk.reload_env()
 # replicated RB+RM+SR epilogue (fused row-panel SpMM + all-gather), three destinations
 for n in (3, 32, 128):
     B = torch.rand(2000, n, device="cuda")
