@@ -181,6 +181,13 @@ int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
     daspmm_csr* h = const_cast<daspmm_csr*>(hc);
     std::lock_guard<std::mutex> lk(h->mu);
     if (h->tile_state != 0) return DASPMM_OK;
+    // Inside a caller's stream capture the build (allocation + synchronisation) cannot
+    // run: that call takes the base walk and a later uncaptured call builds the tiles.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return DASPMM_OK;
+    }
     h->tile_state = -1;
     if (h->dtype != DASPMM_F32 || h->M <= 0 || h->nnz <= 0) return DASPMM_OK;
     static const double min_fill = [] {
