@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace daspmm {
 
@@ -60,6 +61,28 @@ inline cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// Shared-memory carveout of one kernel, set once per process (percent of the unified
+// L1 / shared array; < 0 leaves the driver's choice). Kernels that size their occupancy
+// by static shared memory set it explicitly: left to the driver, the staged tile walk
+// ran at 1 CTA per SM in one process and 5 in another (banded s20 N = 64: 526 vs 180 us,
+// profiles/r02_carveout_probe.txt).
+template <auto K>
+inline void carveout_once(int pct) {
+    static const bool done = [pct] {
+        if (pct >= 0) {
+            cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            cudaGetLastError();
+        }
+        return true;
+    }();
+    (void)done;
+}
+// DASPMM_<NAME>_CARVEOUT override (tuning), read once.
+inline int carveout_env(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
 }
 
 // Launch site of the instantiation tables (`p`, `a`, `s` in scope). A translation unit

@@ -4,16 +4,24 @@
 namespace daspmm {
 // Fast path instantiations (CTA-combined boundary rows); the exact path keeps one
 // partition chunk per group (k_eb_sr) so owned rows match the reference bit for bit.
+// The CTA-combined walk's boundary slots are static shared memory: explicit carveout
+// (DASPMM_CTA_CARVEOUT; default -1 = the driver's choice, being measured).
+#define DASPMM_GO_CTA(K, G, NT)                                                          \
+    do {                                                                                 \
+        static const int carve_ = carveout_env("DASPMM_CTA_CARVEOUT", -1);               \
+        carveout_once<K>(carve_);                                                        \
+        DASPMM_GO(K, G, NT);                                                             \
+    } while (0)
 #define DASPMM_CTA_LPR_TABLE_NT(T, CM, V, NT)                                             \
     switch (p.L) {                                                                        \
-        case 1: DASPMM_GO((k_eb_sr_cta<T, CM, V, 1, 1, NT>), p.grid, NT); break;          \
-        case 2: DASPMM_GO((k_eb_sr_cta<T, CM, V, 2, 1, NT>), p.grid, NT); break;          \
-        case 4: DASPMM_GO((k_eb_sr_cta<T, CM, V, 4, 1, NT>), p.grid, NT); break;          \
-        case 8: DASPMM_GO((k_eb_sr_cta<T, CM, V, 8, 1, NT>), p.grid, NT); break;          \
-        case 16: DASPMM_GO((k_eb_sr_cta<T, CM, V, 16, 1, NT>), p.grid, NT); break;        \
+        case 1: DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 1, 1, NT>), p.grid, NT); break;          \
+        case 2: DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 2, 1, NT>), p.grid, NT); break;          \
+        case 4: DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 4, 1, NT>), p.grid, NT); break;          \
+        case 8: DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 8, 1, NT>), p.grid, NT); break;          \
+        case 16: DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 16, 1, NT>), p.grid, NT); break;        \
         case 32:                                                                          \
-            if (p.X == 2) DASPMM_GO((k_eb_sr_cta<T, CM, V, 32, 2, NT>), p.grid, NT);      \
-            else DASPMM_GO((k_eb_sr_cta<T, CM, V, 32, 1, NT>), p.grid, NT);               \
+            if (p.X == 2) DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 32, 2, NT>), p.grid, NT);      \
+            else DASPMM_GO_CTA((k_eb_sr_cta<T, CM, V, 32, 1, NT>), p.grid, NT);               \
             break;                                                                        \
         default: return cudaErrorNotSupported;                                            \
     }
@@ -49,10 +57,22 @@ DASPMM_SR_LAUNCHER(launch_eb_sr, k_eb_sr)
 
 template <int NT>
 static cudaError_t launch_eb_sr_thr_nt(const Plan& p, const SpmmArgs<float>& a, cudaStream_t s) {
+    // staging of 3 x S x NT words per CTA sizes the occupancy: explicit carveout
+    // (DASPMM_THR_CARVEOUT; default -1 = the driver's choice, being measured)
+    static const int carve = carveout_env("DASPMM_THR_CARVEOUT", -1);
     switch (p.V) {
-        case 1: DASPMM_GO((k_eb_sr_thr<float, false, 1, kThrS, NT>), p.grid, NT); break;
-        case 2: DASPMM_GO((k_eb_sr_thr<float, false, 2, kThrS, NT>), p.grid, NT); break;
-        case 4: DASPMM_GO((k_eb_sr_thr<float, false, 4, kThrS4, NT>), p.grid, NT); break;
+        case 1:
+            carveout_once<k_eb_sr_thr<float, false, 1, kThrS, NT>>(carve);
+            DASPMM_GO((k_eb_sr_thr<float, false, 1, kThrS, NT>), p.grid, NT);
+            break;
+        case 2:
+            carveout_once<k_eb_sr_thr<float, false, 2, kThrS, NT>>(carve);
+            DASPMM_GO((k_eb_sr_thr<float, false, 2, kThrS, NT>), p.grid, NT);
+            break;
+        case 4:
+            carveout_once<k_eb_sr_thr<float, false, 4, kThrS4, NT>>(carve);
+            DASPMM_GO((k_eb_sr_thr<float, false, 4, kThrS4, NT>), p.grid, NT);
+            break;
         default: return cudaErrorNotSupported;
     }
     return cudaGetLastError();

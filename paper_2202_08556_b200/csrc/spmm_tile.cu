@@ -10,10 +10,16 @@ constexpr int kTileThreads = 128;
 // Column slots per panel <= 4: the direct walk; 8..32: the staged, pipelined walk.
 template <int V, int CL, int RL, int U>
 void go_u(const Plan& p, const SpmmArgs<float>& a, const TileArgs& t, cudaStream_t s) {
-    if constexpr (CL <= 4)
+    if constexpr (CL <= 4) {
         k_rb_sr_tile_direct<V, CL, RL, 1, kTileThreads, U><<<p.grid, kTileThreads, 0, s>>>(a, t);
-    else
-        k_rb_sr_tile<V, CL, RL, 1, kTileThreads, U><<<p.grid, kTileThreads, 0, s>>>(a, t);
+    } else {
+        constexpr auto k = k_rb_sr_tile<V, CL, RL, 1, kTileThreads, U>;
+        // 5 CTAs of 32 KB staging per SM (96 registers) need ~70% of the array as shared
+        // memory; 50 and 75 measure the same, 100 costs L1 hits (r02_carveout_probe.txt)
+        static const int carve = carveout_env("DASPMM_TILE_CARVEOUT", 75);
+        carveout_once<k>(carve);
+        k<<<p.grid, kTileThreads, 0, s>>>(a, t);
+    }
 }
 
 template <int V, int CL, int RL>
