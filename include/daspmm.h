@@ -247,7 +247,8 @@ int daspmm_reload_env(void);
  *   rows, 3 = EB+SR one-lane staged sub-chunks (*param = pairs per thread), 4 = lean
  *   SR kernel (*param = rows per group for RB, pairs per chunk for EB), 5 = EB+SR with
  *   TMA gather4 B-row fetches (*param = pairs per warp), 6 = RB+RM+SR on the handle's
- *   dense 8-row panel tiles (*param = row lanes per panel: 8 narrow N, 1 wide N).
+ *   dense 8-row panel tiles (*param = row lanes per panel: 8 narrow N, 1 wide N), 7 =
+ *   RB+CM+SR with lanes over rows (*param = columns per block).
  * Diagnostics for tests and the bench's per-call report. */
 int daspmm_plan_info(const daspmm_csr* csr, int kernel, int64_t N, const void* d_B, int64_t ldb,
                      const void* d_C, int64_t ldc, unsigned flags, int* variant, int64_t* param);

@@ -150,6 +150,8 @@ struct Knobs {
     bool pdl = true;          // DASPMM_PDL=0: EB kernels wait for their prologue to finish
     bool tile = true;         // DASPMM_TILE=0: no dense row-panel tile walk for RB+RM+SR
     bool tile_force = false;  // DASPMM_TILE=2: the tile walk at any grid size (tests)
+    bool cm_rows = true;      // DASPMM_CM_ROWS=0: RB+CM+SR on the base walk (lanes over columns)
+    bool cm_rows_force = false;  // DASPMM_CM_ROWS=2: lanes over rows on skewed rows too (tests)
     int tile_rl = 0;          // DASPMM_TILE_RL=1/8: force the tile walk's row lanes (tuning)
     int tile_u = 0;           // DASPMM_TILE_U=2/4/8: B rows in flight per lane (tuning)
     // DASPMM_CTA_THREADS (64/128/256): CTA size of the CTA-combined EB walk. Measured:
@@ -191,6 +193,8 @@ static Knobs read_knobs() {
     k.pdl = !on("DASPMM_PDL", '0');
     k.tile = !on("DASPMM_TILE", '0');
     k.tile_force = on("DASPMM_TILE", '2');
+    k.cm_rows = !on("DASPMM_CM_ROWS", '0');
+    k.cm_rows_force = on("DASPMM_CM_ROWS", '2');
     k.tile_rl = int(i64("DASPMM_TILE_RL"));
     if (const int64_t u = i64("DASPMM_TILE_U"); u == 2 || u == 4 || u == 8) k.tile_u = int(u);
     if (const int64_t t = i64("DASPMM_CTA_THREADS"); t == 32 || t == 64 || t == 128 || t == 256) {
@@ -437,6 +441,22 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && !p.lean)
             p.rb_threads = kn.rb_threads;
         workers = (h->M + rpg - 1) / rpg;
+        // RB+CM+SR: lanes over rows (spmm_cm.cu) — a warp's 32 rows read one column of B
+        // together, coalesced wherever neighbouring rows share columns (banded s20 N = 128
+        // 9.1 -> 1.6 ms, uniform 41.7 -> 8.8 ms). Skewed rows keep the base walk: a lane
+        // alone on a long row stalls its warp (power-law s20 N = 32 6.8 -> 18.0 ms;
+        // profiles/r02_cm_rows_probe.txt).
+        const double sd_rows = h->M > 0 ? std::sqrt(h->h_feat.ss_par / double(h->M)) : 0.0;
+        const double avg_rows = h->M > 0 ? double(h->nnz) / double(h->M) : 0.0;
+        if (!base_only && !exact && p.cm && h->dtype == DASPMM_F32 && P <= 0 && kn.cm_rows &&
+            (sd_rows <= 2.0 * avg_rows || kn.cm_rows_force)) {
+            p.cm_rows = true;
+            p.L = int(std::min<int64_t>(8, pow2_ceil(N)));
+            p.V = 1;
+            p.X = 1;
+            p.grid = dim3(unsigned((h->M + 127) / 128), unsigned((N + p.L - 1) / p.L), 1);
+            return p;
+        }
         // Row-local matrices with tiles at least half full: the dense row-panel tile walk
         // (tile.cuh) gathers each B row once per 8-row panel instead of once per nonzero
         // (banded s20: N = 2 43 -> 31 us, N = 32 156 -> 114, half-width 32 N = 128 1749 ->
@@ -512,6 +532,7 @@ static cudaError_t run_plan(const daspmm_csr* h, const Plan& p, int64_t W, const
     const bool eb = p.kernel >= 4, pr = p.kernel & 1;
     if constexpr (std::is_same<T, float>::value) {
         if (p.tile) return launch_rb_sr_tile(p, a, h->tile_off, h->tile_c0, h->tile_val, h->n_pan, s);
+        if (p.cm_rows) return launch_rb_cm_rows(p, a, s);
         if (p.tma) {  // prologue: split rows at warp-range ends and empty rows
             cudaError_t e = launch_eb_prep_uniform<T>(h->coo_rows, h->nnz, p.sub, p.P, 1,
                                                       static_cast<T*>(C), ldc, int(N),
@@ -1109,8 +1130,8 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
     if (kernel == 0 && !(flags & DASPMM_EXACT))
         if (int rc = ensure_tiles(h, 0)) return rc;
     const Plan p = plan_spmm(h, kernel, 0, 8, N, B, ldb, C, ldc, (flags & DASPMM_EXACT) != 0);
-    *variant = p.tile ? 6 : p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
-    *param = p.tile ? p.tile_rl
+    *variant = p.cm_rows ? 7 : p.tile ? 6 : p.win_rows > 0 ? 1 : p.cta ? 2 : p.thr ? 3 : p.lean ? 4 : p.tma ? 5 : 0;
+    *param = p.cm_rows ? p.L : p.tile ? p.tile_rl
              : p.win_rows > 0 ? p.win_rows : (p.thr || p.tma || (p.lean && kernel >= 4)) ? p.sub
              : p.lean ? p.rpg : int64_t(p.grid.y);
     return DASPMM_OK;

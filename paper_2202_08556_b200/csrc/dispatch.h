@@ -38,6 +38,7 @@ struct Plan {
     bool tile = false;   // RB+RM+SR on the handle's dense row-panel tiles (tile.cuh)
     int tile_rl = 1;     // ... row lanes per panel (1 or kTileRows); L = column lanes
     int tile_u = 2;      // ... tile columns (B rows) in flight per lane (2, 4 or 8)
+    bool cm_rows = false;  // RB+CM+SR with lanes over rows (spmm_cm.cu); L = columns per block
 };
 
 // Kernel launch; with pdl, programmatic stream serialization: the kernel may start while
@@ -119,6 +120,8 @@ template <typename T> cudaError_t launch_eb_pr(const Plan&, const SpmmArgs<T>&, 
 // RB+RM+SR on dense row-panel tiles (spmm_tile.cu); p.L column lanes x p.tile_rl rows.
 cudaError_t launch_rb_sr_tile(const Plan&, const SpmmArgs<float>&, const int* off, const int* c0,
                               const float* val, int64_t n_pan, cudaStream_t);
+// RB+CM+SR, lanes over rows, p.L columns per grid.y block (spmm_cm.cu).
+cudaError_t launch_rb_cm_rows(const Plan&, const SpmmArgs<float>&, cudaStream_t);
 // PR groups wider than a warp (W = 64 .. 1024), RB and EB (spmm_pr_wide.cu).
 template <typename T> cudaError_t launch_pr_wide(const Plan&, const SpmmArgs<T>&, cudaStream_t);
 template <typename T>

@@ -444,16 +444,19 @@ def reload_env():
 
 
 PLAN_VARIANTS = {0: "base", 1: "rb_window", 2: "eb_cta", 3: "eb_thread", 4: "lean", 5: "eb_tma",
-                 6: "rb_tile"}
+                 6: "rb_tile", 7: "cm_rows"}
 
 
-def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False):
-    """(variant name, parameter) of the launch daspmm_spmm would run for these
-    row-major device operands — diagnostics (see daspmm_plan_info)."""
+def plan_info(kernel, a: DeviceCsr, B, C_out, exact: bool = False, b_layout: Layout = None):
+    """(variant name, parameter) of the launch daspmm_spmm would run for these device
+    operands — diagnostics (see daspmm_plan_info). B as for spmm_device: K x N row-major,
+    or the N x K buffer of a column-major B (the default for CM kernels)."""
     kid = kernel.index() if isinstance(kernel, KernelId) else int(kernel)
-    _check_operands(a, B, C_out, Layout.RowMajor, "plan_info")
+    if b_layout is None:
+        b_layout = Layout.ColMajor if (kid >> 1) & 1 else Layout.RowMajor
+    n = _check_operands(a, B, C_out, b_layout, "plan_info")
     v, prm = C.c_int(), C.c_int64()
-    check(lib().daspmm_plan_info(a._h, kid, B.shape[1], B.data_ptr(), _ld(B), C_out.data_ptr(),
+    check(lib().daspmm_plan_info(a._h, kid, n, B.data_ptr(), _ld(B), C_out.data_ptr(),
                                  _ld(C_out), _lib.EXACT if exact else 0, C.byref(v),
                                  C.byref(prm)))
     return PLAN_VARIANTS[v.value], prm.value

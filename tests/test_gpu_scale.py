@@ -112,9 +112,12 @@ VARIANTS = [
     ("suite", "banded_s20_b8", 2, 0, {}, "rb_tile"),            # direct walk, lane per row
     ("suite", "banded_s20_b8", 33, 0, {}, "rb_tile"),           # V = 1, two column tiles
     ("suite", "banded_s20_b8", 2, 4, {}, "eb_thread"),
-    ("suite", "uniform_s17_d16", 8, 2, {}, "base"),             # CM kernels (col-major B)
+    ("suite", "uniform_s17_d16", 8, 2, {}, "cm_rows"),          # CM kernels (col-major B)
+    ("suite", "banded_s17_b8", 128, 2, {}, "cm_rows"),
+    ("suite", "uniform_s17_d16", 8, 2, {"DASPMM_CM_ROWS": "0"}, "base"),
+    ("suite", "powerlaw_s17_d16", 32, 2, {}, "base"),           # skewed rows: base CM walk
     ("suite", "uniform_s17_d16", 8, 3, {}, "base"),
-    ("suite", "powerlaw_s17_d16", 8, 6, {}, "base"),
+    ("suite", "powerlaw_s17_d16", 8, 6, {}, "eb_cta"),
     ("suite", "powerlaw_s17_d16", 8, 7, {}, "base"),
     ("c3", "c3_reddit_like", 128, 4, {}, "lean"),               # segment walk, long rows
 ]
@@ -134,9 +137,8 @@ def test_launch_variants_at_scale(env, case):
         cm = (kid >> 1) & 1
         Bop = B.t().contiguous() if cm else B
         C = torch.full((M, n), float("nan"), device="cuda")
-        if not cm:
-            variant, _ = sk.plan_info(kid, d, B, C)
-            assert variant == want, (case, variant)
+        variant, _ = sk.plan_info(kid, d, Bop, C)
+        assert variant == want, (case, variant)
         sk.spmm_device(kid, d, Bop, C)
         torch.cuda.synchronize()
         res = S.check(rp, ci, va, K, Bop if cm else B, C, S.sample_rows(rp_h, seed=kid + n),
