@@ -84,11 +84,19 @@ int daspmm_csr_create_host(int64_t num_rows, int64_t num_cols, int64_t nnz,
                            const void* values, int dtype, daspmm_csr** out);
 
 /* Adopts (copy == 0: borrows, caller keeps ownership) or copies (copy != 0) a CSR
- * already in device memory with int32 offsets and columns. */
+ * already in device memory with int32 offsets and columns. A borrowed structure must not
+ * change while the handle lives (features, empty rows, column windows and COO row ids
+ * are derived from it); values may change in place if the caller then calls
+ * daspmm_csr_values_updated (the row-panel tiles hold a copy of the values). */
 int daspmm_csr_create_device(int64_t num_rows, int64_t num_cols, int64_t nnz,
                              const int32_t* d_row_offsets, const int32_t* d_col_indices,
                              const void* d_values, int dtype, int copy, daspmm_stream stream,
                              daspmm_csr** out);
+
+/* The values of a borrowed CSR were changed in place (same structure): drops the
+ * handle's derived copies of the values (row-panel tiles, rebuilt on the next call that
+ * uses them). Synchronises the handle's device first. */
+int daspmm_csr_values_updated(daspmm_csr* csr);
 
 /* Row panel [r0, r1) of an existing handle (offsets rebased, columns shared) — the
  * multi-GPU layer's unit. Device-to-device copy on `stream`. */

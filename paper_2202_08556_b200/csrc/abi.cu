@@ -927,6 +927,22 @@ int daspmm_csr_create_panel(const daspmm_csr* full, int64_t r0, int64_t r1, dasp
     return finish_create(h, s, out);
 }
 
+int daspmm_csr_values_updated(daspmm_csr* h) {
+    if (!h) return fail(DASPMM_ERR_INVALID_ARG, "csr_values_updated: null handle");
+    DeviceGuard g(h->device);
+    cudaError_t e = cudaDeviceSynchronize();  // no kernel may still read the old tiles
+    if (e != cudaSuccess) return cuda_fail(e, "csr_values_updated");
+    std::lock_guard<std::mutex> lk(h->mu);
+    cudaFree(h->tile_off);
+    cudaFree(h->tile_c0);
+    cudaFree(h->tile_val);
+    h->tile_off = h->tile_c0 = nullptr;
+    h->tile_val = nullptr;
+    h->n_pan = 0;
+    h->tile_state = 0;
+    return DASPMM_OK;
+}
+
 int daspmm_csr_destroy(daspmm_csr* h) {
     if (!h) return DASPMM_OK;
     graph_cache_free(h);

@@ -280,6 +280,11 @@ class DeviceCsr:
         keep = None if copy else (row_offsets, col_indices, values)
         return DeviceCsr(out.value, dtype, keep, row_offsets.device.index)
 
+    def values_updated(self):
+        """The borrowed values tensor was changed in place (same structure): drop the
+        handle's derived copies of the values (daspmm_csr_values_updated)."""
+        check(lib().daspmm_csr_values_updated(self._h))
+
     def panel(self, r0: int, r1: int, stream=None) -> "DeviceCsr":
         out = C.c_void_p()
         check(lib().daspmm_csr_create_panel(self._h, r0, r1, _stream_ptr(stream), C.byref(out)))

@@ -240,3 +240,24 @@ def test_tiles_through_da_spmm(sk):
         assert (err <= H.gamma_bound(a, x64, np.float32)).all()
     os.environ.pop("DASPMM_TILE", None)
     sk.reload_env()
+
+
+def test_tiles_follow_values_updated(sk):
+    """A borrowed CSR whose values change in place: after values_updated() the tile walk
+    uses the new values (the tiles are a copy)."""
+    import torch
+
+    from paper_2202_08556_b200 import gen
+
+    M, K, rp, ci, va = gen.banded(1 << 17, 8, seed=9)
+    d = sk.DeviceCsr.from_device(M, K, rp, ci, va)  # borrows va
+    B = torch.rand(K, 32, device="cuda")
+    C1 = torch.empty(M, 32, device="cuda")
+    sk.spmm_device(0, d, B, C1)
+    assert sk.plan_info(0, d, B, C1)[0] == "rb_tile"
+    va.mul_(-2.0)  # exact in fp32
+    d.values_updated()
+    C2 = torch.empty(M, 32, device="cuda")
+    sk.spmm_device(0, d, B, C2)
+    torch.cuda.synchronize()
+    assert torch.equal(C2, -2.0 * C1)
