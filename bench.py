@@ -164,8 +164,9 @@ def build_suite(small: bool, rank: int, world: int, workload: str = "suite"):
 def _setup_costs(mats):
     """Handle-creation cost per matrix (not in any timed SpMM): device arrays adopted
     (features, empty rows, K_touched, column windows: daspmm_csr_create_device), host int64
-    arrays uploaded and validated / compacted on the device (daspmm_csr_create_host), the
-    COO row ids built on first EB use, and extract_features' exact std_row replay."""
+    arrays uploaded and validated / compacted on the device (daspmm_csr_create_host),
+    extract_features' exact std_row replay, and what the first calls build lazily (COO
+    row ids; the row-panel tiles where they pay)."""
     import numpy as np
     import torch
 
@@ -177,7 +178,9 @@ def _setup_costs(mats):
         ci = m["ci"].cpu().numpy().astype(np.int64)
         va = m["va"].cpu().numpy()
         a = sk.CsrMatrix(m["M"], m["K"], rp, ci, va, np.float32)
-        t_host, t_feat = [], []
+        t_host, t_feat, t_lazy = [], [], []
+        B = torch.zeros(m["K"], 32, device="cuda")
+        Cb = torch.empty(m["M"], 32, device="cuda")
         for _ in range(3):  # median of 3: single host-side timings vary with the box
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -187,11 +190,24 @@ def _setup_costs(mats):
             t0 = time.perf_counter()
             sk.extract_features(h, 32)
             t_feat.append((time.perf_counter() - t0) * 1e3)
+            # lazily built structures on the first calls (COO row ids, row-panel tiles):
+            # first RB+RM+SR and EB+RM+SR calls minus the same calls again
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sk.spmm_device(0, h, B, Cb)
+            sk.spmm_device(4, h, B, Cb)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            sk.spmm_device(0, h, B, Cb)
+            sk.spmm_device(4, h, B, Cb)
+            torch.cuda.synchronize()
+            t_lazy.append(((t1 - t0) - (time.perf_counter() - t1)) * 1e3)
             h.close()
-        t_host, t_feat = sorted(t_host)[1], sorted(t_feat)[1]
+        t_host, t_feat, t_lazy = sorted(t_host)[1], sorted(t_feat)[1], sorted(t_lazy)[1]
         out[m["name"]] = {"from_device_ms": round(m.get("handle_ms", 0.0), 3),
                           "from_host_ms": round(t_host, 3),
                           "extract_features_exact_ms": round(t_feat, 3),
+                          "first_call_lazy_build_ms": round(t_lazy, 3),
                           "rows": m["M"], "nnz": m["nnz_total"]}
         del a, rp, ci, va
     return out
@@ -342,15 +358,19 @@ def run_ours(args):
         pass
 
     # ---- e2e: host operands through the public API (pinned H2D, DA-SpMM, D2H)
-    if sum(c["B"].numel() + c["C"].numel() for c in calls) * 4 > (16 << 30):
+    e2e = parity = warm = overhead = batched = setup = None
+    if args.profile_step:
+        pass  # --profile-step: only the warm-up and the timed steps (ncu launch lists)
+    elif sum(c["B"].numel() + c["C"].numel() for c in calls) * 4 > (16 << 30):
         e2e = None  # operands too large to stage in pinned host memory (c5: 68 GB)
     else:
         e2e = _e2e(calls, one, stream, args, world, total_flops)
-    parity = _parity_map(calls) if rank == 0 else None
-    warm = _warm(calls, one, stream, world, dev, total_flops)
-    overhead = _da_overhead(calls, model, stream, flush) if rank == 0 else None
-    batched = _batched_small(calls, model, flush, per_call_ms) if rank == 0 else None
-    setup = _setup_costs(mats) if rank == 0 and world == 1 else None
+    if not args.profile_step:
+        parity = _parity_map(calls) if rank == 0 else None
+        warm = _warm(calls, one, stream, world, dev, total_flops)
+        overhead = _da_overhead(calls, model, stream, flush) if rank == 0 else None
+        batched = _batched_small(calls, model, flush, per_call_ms) if rank == 0 else None
+        setup = _setup_costs(mats) if rank == 0 and world == 1 else None
     assembly = None
     if world > 1:
         try:
@@ -1042,9 +1062,14 @@ def main():
     ap.add_argument("--ns", default="")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="only the warm-up and the timed steps (for ncu launch lists); "
+                         "implies --no-cpu --no-cusparse")
     ap.add_argument("--roofline-table", default="",
                     help="also write a per-call roofline table (markdown) to this path")
     args = ap.parse_args()
+    if args.profile_step:
+        args.no_cpu = args.no_cusparse = True
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

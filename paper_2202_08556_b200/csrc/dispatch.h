@@ -71,14 +71,17 @@ inline cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block
 // profiles/r02_carveout_probe.txt).
 template <auto K>
 inline void carveout_once(int pct) {
-    static const bool done = [pct] {
-        if (pct >= 0) {
-            cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-            cudaGetLastError();
-        }
-        return true;
-    }();
-    (void)done;
+    if (pct < 0) return;
+    static bool done[64] = {};  // per device: function attributes are set per context
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return;
+    }
+    if (done[dev]) return;
+    cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+    done[dev] = true;
 }
 // DASPMM_<NAME>_CARVEOUT override (tuning), read once.
 inline int carveout_env(const char* name, int dflt) {

@@ -1,5 +1,11 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel
-family: launches, total time and share. python tools/launch_summary.py launches.csv"""
+family: launches, total time and share.
+
+python tools/launch_summary.py launches.csv [--ours] [--step]
+  --ours  only this library's kernels
+  --step  only the kernels an SpMM call launches (design-point kernels, EB prologues,
+          the selector), not handle creation / lazy set-up (features, column windows,
+          COO row ids, tiles, the exact std_row replay)"""
 import csv
 import io
 import re
@@ -24,8 +30,12 @@ def main():
                  "ms": 1e3}.get(unit.strip(), 1.0)
         agg[fam][0] += 1
         agg[fam][1] += v * scale
-    if "--ours" in sys.argv:  # only this library's kernels (the DA-SpMM step)
+    if "--ours" in sys.argv or "--step" in sys.argv:  # only this library's kernels
         agg = {k: v for k, v in agg.items() if k.startswith("daspmm::")}
+    if "--step" in sys.argv:
+        setup = ("k_row_terms", "k_cols_touched", "k_popcount", "k_fine_spans", "k_coo_rows",
+                 "k_tile_spans", "k_tile_fill", "k_std_sequential", "k_ingest", "k_rebase")
+        agg = {k: v for k, v in agg.items() if not any(f"::{n}" in k for n in setup)}
     tot = sum(v[1] for v in agg.values()) or 1.0
     print(f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}")
     for fam, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):

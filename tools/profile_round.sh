@@ -9,7 +9,7 @@ tag=${1:-r01}
 out=gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file $out/launches_$tag.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu --no-cusparse > $out/bench_under_ncu_$tag.json 2>&1
+    python bench.py --steps 1 --warmup 3 --profile-step > $out/bench_under_ncu_$tag.json 2>&1
 [ "${2:-}" = "full" ] || exit 0
 echo "{" > $out/ncu_${tag}_traffic.json
 first=1
@@ -17,7 +17,8 @@ first=1
 for spec in "k_rb_sr uniform_s20_d16 128 0" "k_eb_sr_cta powerlaw_s20_d16 128 4" \
             "k_eb_sr_lean_rw powerlaw_s20_d16 16 4" "k_eb_sr_thr uniform_s20_d16 2 4" \
             "k_rb_sr banded_s20_b8 128 0" "k_eb_sr_lean c3_reddit_like 128 4 c3" \
-            "k_eb_prep_uniform powerlaw_s20_d16 64 4"; do
+            "k_eb_prep_uniform powerlaw_s20_d16 64 4" "k_rb_sr_tile banded_s20_b8 128 0" \
+            "k_rb_sr_tile_direct banded_s20_b8 16 0"; do
   set -- $spec
   wl=${5:-suite}
   case_name="$2/N$3"
