@@ -467,6 +467,9 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             const int64_t nvt = (std::min<int64_t>(N, 128) + p.V - 1) / p.V;  // slots per tile
             const int cl = pow2_ceil(nvt);
             int rl = cl == 1 ? 8 : 1;  // one column slot (N <= 4): a lane per row
+            // narrow N on a grid too small for one lane per column slot: a lane per row
+            // (banded s17 N = 8: 18.4 -> 12.3 us)
+            if (cl <= 4 && h->n_pan * cl * rl < 65536) rl = 8;
             if (kn.tile_rl == 1 || (kn.tile_rl == 8 && cl <= 4)) rl = kn.tile_rl;  // tuning
             const int64_t thr = h->n_pan * cl * rl;
             if (thr >= 65536 || kn.tile_force) {
