@@ -475,13 +475,11 @@ def _da_overhead(calls, model, stream, flush, reps=3):
         kid = int(c["kout"].item())
         sk.spmm_selected(c["d"], model, c["B"], c["C"], kernel_out=c["kout"], stream=stream,
                          reselect=True)  # builds the reselect graph outside the timing
-        resel += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"],
-                                                kernel_out=c["kout"], stream=stream,
+        resel += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"], stream=stream,
                                                 reselect=True))
-        direct += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"],
-                                                 kernel_out=c["kout"], stream=stream))
-        Bk = c["B"].t().contiguous() if (kid >> 1) & 1 else c["B"]
-        plain += timed(lambda: sk.spmm_device(kid, c["d"], Bk, c["C"], stream=stream))
+        direct += timed(lambda: sk.spmm_selected(c["d"], model, c["B"], c["C"], stream=stream))
+        # what DA-SpMM runs on this row-major B: the choice, or its layout twin for CM
+        plain += timed(lambda: sk.spmm_device(kid & ~2, c["d"], c["B"], c["C"], stream=stream))
     n = len(calls)
     return {"reselect_ms_per_step": round(resel, 4), "direct_ms_per_step": round(direct, 4),
             "plain_kernel_ms_per_step": round(plain, 4),
@@ -490,7 +488,7 @@ def _da_overhead(calls, model, stream, flush, reps=3):
             "note": "reselect = device selector walk + graph SWITCH + kernel every call "
                     "(the reference's per-call predict_kernel flow, spmmkit_cli.cpp:239-270); "
                     "direct = published choice launched directly; plain = daspmm_spmm of the "
-                    "same kernel (CM kernels on a pre-transposed B)"}
+                    "kernel that runs (a CM choice runs its RM layout twin on the row-major B)"}
 
 
 def _parity_map(calls):

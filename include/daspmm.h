@@ -61,7 +61,14 @@ enum {
     /* daspmm_spmm_selected only: run the device selector (ensemble walk) and the SWITCH
      * dispatch on this call even when the choice for (matrix, model, N, hw) is already
      * known — measures the uncached DA-SpMM overhead. */
-    DASPMM_RESELECT = 2u
+    DASPMM_RESELECT = 2u,
+    /* daspmm_spmm_selected only: when the chosen design point needs the other layout of
+     * B, convert B on the device first, as the reference's spmm_auto_layout does
+     * (spmm.hpp:275-281). Default: run the chosen point's layout twin on B as given (same
+     * M- and K-loop choices; for SR the same fmaf sequence, so the same bits) and save
+     * the O(K N) conversion — the selector is trained on kernels timed with B already in
+     * their layout, so the conversion is not part of what it weighs. */
+    DASPMM_CONVERT_LAYOUT = 4u
 };
 
 /* Human-readable message for the last failing call on this thread. */
@@ -182,8 +189,9 @@ int daspmm_select(const daspmm_csr* csr, const daspmm_model* model, int64_t n_co
 
 /* DA-SpMM: device selector + device-side dispatch (CUDA graph with a SWITCH
  * conditional node; the selector kernel sets the branch). B may be in either
- * layout; a body whose kernel needs the other layout converts B on the device
- * first, as spmm_auto_layout does. W/Cb from make_config(kernel, N) defaults
+ * layout; a choice that needs the other layout runs its layout twin on B as given,
+ * or, with DASPMM_CONVERT_LAYOUT, converts B on the device first as spmm_auto_layout
+ * does. d_kernel reports the selector's choice. W/Cb from make_config(kernel, N) defaults
  * (worker.hpp:47-55) unless W > 0. Optional d_kernel receives the choice.
  * Caching: the choice depends only on (matrix, model, N, hw). Until the device has
  * published it, calls run the graph (at most 4 instantiated graphs per handle, LRU);

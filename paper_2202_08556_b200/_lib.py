@@ -24,6 +24,7 @@ F32, F64 = 0, 1
 ROW_MAJOR, COL_MAJOR = 0, 1
 EXACT = 1
 RESELECT = 2
+CONVERT_LAYOUT = 4
 SPLIT_AUTO, SPLIT_ROWS, SPLIT_COLS = -1, 0, 1
 
 _vp = C.c_void_p

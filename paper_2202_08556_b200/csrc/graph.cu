@@ -172,10 +172,12 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
     }
     if ((e = cudaMalloc(&en.chunk_row, sizeof(int) * size_t(max_p))) != cudaSuccess)
         return cuda_fail(e, "graph: cudaMalloc(chunk_row)");
+    // B in the other layout only when the caller asks for the reference's conversion;
+    // otherwise a body whose kernel needs it runs the layout twin (below).
     const size_t bt_bytes = size_t(elem(h->dtype)) * size_t(h->K) * size_t(k.N);
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    if (bt_bytes > 0 && bt_bytes <= free_b / 4) {
+    if ((k.flags & DASPMM_CONVERT_LAYOUT) && bt_bytes > 0 && bt_bytes <= free_b / 4) {
         if ((e = cudaMalloc(&en.bt, bt_bytes)) != cudaSuccess) en.bt = nullptr;
     }
     const int64_t ldt = k.b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
@@ -253,8 +255,8 @@ static int build_entry(const daspmm_csr* h, const daspmm_model* m, const Key& k,
             ldk = ldt;
         }
         // make_config defaults (worker.hpp:47-55): W = 8 unless given.
-        rc = e == cudaSuccess ? spmm_device(h, run_kid, 0, k.W, Bk, ldk, k.N, k.C, k.ldc, k.flags,
-                                            cap, en.chunk_row)
+        rc = e == cudaSuccess ? spmm_device(h, run_kid, 0, k.W, Bk, ldk, k.N, k.C, k.ldc,
+                                            k.flags & DASPMM_EXACT, cap, en.chunk_row)
                               : cuda_fail(e, "graph: transpose");
         cudaGraph_t bo = nullptr;
         e = cudaStreamEndCapture(cap, &bo);
@@ -361,18 +363,21 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
         e = cudaMemcpyAsync(d_kernel, pinned_ids() + decided, sizeof(int), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm_selected: kernel id");
     const int want = ((decided >> 1) & 1) ? DASPMM_COL_MAJOR : DASPMM_ROW_MAJOR;
-    if (want == b_layout) return spmm_device(h, decided, 0, W, d_B, ldb, N, d_C, ldc, kflags, s, nullptr);
+    const unsigned xflags = kflags & DASPMM_EXACT;
+    if (want == b_layout) return spmm_device(h, decided, 0, W, d_B, ldb, N, d_C, ldc, xflags, s, nullptr);
+    if (!(kflags & DASPMM_CONVERT_LAYOUT))  // the layout twin on B as given
+        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, xflags, s, nullptr);
     const size_t bytes = size_t(elem(h->dtype)) * size_t(h->K) * size_t(N);
     void* bt = nullptr;
     if (scratch_alloc(&bt, std::max<size_t>(bytes, 16), h->device, s) != cudaSuccess) {
         cudaGetLastError();  // no room for the other layout: the layout twin (same M/K choices)
-        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, kflags, s, nullptr);
+        return spmm_device(h, decided ^ 2, 0, W, d_B, ldb, N, d_C, ldc, xflags, s, nullptr);
     }
     const int64_t ldt = b_layout == DASPMM_ROW_MAJOR ? std::max<int64_t>(h->K, 1)
                                                      : std::max<int64_t>(N, 1);
     e = b_layout == DASPMM_ROW_MAJOR ? transpose(h->dtype, d_B, h->K, N, ldb, bt, ldt, s)
                                      : transpose(h->dtype, d_B, N, h->K, ldb, bt, ldt, s);
-    int rc = e == cudaSuccess ? spmm_device(h, decided, 0, W, bt, ldt, N, d_C, ldc, kflags, s, nullptr)
+    int rc = e == cudaSuccess ? spmm_device(h, decided, 0, W, bt, ldt, N, d_C, ldc, xflags, s, nullptr)
                               : cuda_fail(e, "transpose");
     scratch_free(bt, s);
     return rc;

@@ -549,16 +549,19 @@ def select_device(a: DeviceCsr, model: SelectorModel, n_cols: int, out, hw: int 
 
 def spmm_selected(a: DeviceCsr, model: SelectorModel, B, C_out, b_layout=Layout.RowMajor,
                   W: int = 8, hw: int = -1, exact: bool = False, kernel_out=None, stream=None,
-                  reselect: bool = False):
+                  reselect: bool = False, convert_layout: bool = False):
     """DA-SpMM: device selector + on-device dispatch (graph SWITCH node). Once the
     device has published its choice for (matrix, model, N, hw), calls launch the chosen
-    kernel directly; ``reselect`` forces the selector + SWITCH path on this call."""
+    kernel directly; ``reselect`` forces the selector + SWITCH path on this call. A choice
+    that needs the other layout of B runs its layout twin on B as given, or converts B
+    first with ``convert_layout`` (the reference's spmm_auto_layout)."""
     b_layout = Layout(b_layout)
     n = _check_operands(a, B, C_out, b_layout, "spmm_selected")
     if kernel_out is not None and (not kernel_out.is_cuda or str(kernel_out.dtype) != "torch.int32"):
         raise InvalidArgument(_lib.ERR_INVALID_ARG, "spmm_selected: kernel_out must be a CUDA int32 tensor")
     kp = kernel_out.data_ptr() if kernel_out is not None else None
-    flags = (_lib.EXACT if exact else 0) | (_lib.RESELECT if reselect else 0)
+    flags = (_lib.EXACT if exact else 0) | (_lib.RESELECT if reselect else 0) | \
+        (_lib.CONVERT_LAYOUT if convert_layout else 0)
     check(lib().daspmm_spmm_selected(a._h, model._m, hw, B.data_ptr(), int(b_layout), _ld(B), n,
                                      C_out.data_ptr(), _ld(C_out), W, flags, kp,
                                      _stream_ptr(stream)))

@@ -347,9 +347,12 @@ def test_graph_dispatch_runs_the_selected_kernel(sk):
                 B = torch.from_numpy(np.ascontiguousarray(x if layout == sk.Layout.RowMajor
                                                           else x.T)).cuda()
                 kout = torch.full((1,), -1, dtype=torch.int32, device="cuda")
-                for rep in range(3):
+                # rep 0-2: layout twin on B as given (default); 3-5: the reference's
+                # conversion of B to the chosen kernel's layout (DASPMM_CONVERT_LAYOUT)
+                for rep in range(6):
                     Cc = torch.full((6000, n), float("nan"), device="cuda")
-                    sk.spmm_selected(d, model, B, Cc, b_layout=layout, kernel_out=kout)
+                    sk.spmm_selected(d, model, B, Cc, b_layout=layout, kernel_out=kout,
+                                     convert_layout=rep >= 3)
                     torch.cuda.synchronize()
                     y = Cc.cpu().numpy().astype(np.float64)
                     assert (np.abs(y - y64) <= bound).all(), (n, layout, rep)
