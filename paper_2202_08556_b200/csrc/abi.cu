@@ -462,7 +462,8 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
         // (banded s20: N = 2 43 -> 31 us, N = 32 156 -> 114, half-width 32 N = 128 1749 ->
         // 889). Grids under ~3.5 CTAs per SM keep the base walk (banded s14 runs 0.5-0.8x
         // on tiles: too few panels to hide the window walk's latency).
-        if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 && h->tile_state == 1 &&
+        if (!base_only && !exact && !p.cm && h->dtype == DASPMM_F32 &&
+            h->tile_state.load(std::memory_order_acquire) == 1 &&
             P <= 0 && kn.tile) {
             const int64_t nvt = (std::min<int64_t>(N, 128) + p.V - 1) / p.V;  // slots per tile
             const int cl = pow2_ceil(nvt);
@@ -942,7 +943,7 @@ int daspmm_csr_values_updated(daspmm_csr* h) {
     h->tile_off = h->tile_c0 = nullptr;
     h->tile_val = nullptr;
     h->n_pan = 0;
-    h->tile_state = 0;
+    h->tile_state.store(0, std::memory_order_release);
     return DASPMM_OK;
 }
 

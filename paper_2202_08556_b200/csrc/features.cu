@@ -180,7 +180,7 @@ __global__ void k_tile_fill(const int* __restrict__ rp, const int* __restrict__ 
 int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
     daspmm_csr* h = const_cast<daspmm_csr*>(hc);
     std::lock_guard<std::mutex> lk(h->mu);
-    if (h->tile_state != 0) return DASPMM_OK;
+    if (h->tile_state.load(std::memory_order_acquire) != 0) return DASPMM_OK;
     // Inside a caller's stream capture the build (allocation + synchronisation) cannot
     // run: that call takes the base walk and a later uncaptured call builds the tiles.
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -188,7 +188,7 @@ int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
         cudaGetLastError();
         return DASPMM_OK;
     }
-    h->tile_state = -1;
+    h->tile_state.store(-1, std::memory_order_relaxed);
     if (h->dtype != DASPMM_F32 || h->M <= 0 || h->nnz <= 0) return DASPMM_OK;
     static const double min_fill = [] {
         const char* e = getenv("DASPMM_TILE_FILL");
@@ -250,7 +250,7 @@ int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
     if ((e = cudaGetLastError()) == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "tiles: fill");
     h->n_pan = n_pan;
-    h->tile_state = 1;
+    h->tile_state.store(1, std::memory_order_release);
     return DASPMM_OK;
 }
 

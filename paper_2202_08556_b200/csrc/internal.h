@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -71,7 +72,10 @@ struct daspmm_csr {
     // Dense row-panel tiles of 8 rows (tile.cuh), fp32 only, built on the first fast
     // RB+RM+SR call (ensure_tiles) when rows are column-sorted and the tiles are at least
     // half full: tile_off[n_pan + 1] (floats), tile_c0[n_pan], tile_val (k-major tiles).
-    int tile_state = 0;  // 0 not examined, 1 built, -1 not worth it
+    // 0 not examined, 1 built, -1 not worth it. Written under mu (ensure_tiles), read
+    // without it by the planner: release / acquire so a reader that sees 1 sees the
+    // arrays below.
+    std::atomic<int> tile_state{0};
     int64_t n_pan = 0;
     double tile_fill = 0.0;
     int32_t* tile_off = nullptr;
