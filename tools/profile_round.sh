@@ -16,9 +16,9 @@ first=1
 # kernel-regex  matrix  N  kernel-id  [workload]
 for spec in "k_rb_sr uniform_s20_d16 128 0" "k_eb_sr_cta powerlaw_s20_d16 128 4" \
             "k_eb_sr_lean_rw powerlaw_s20_d16 16 4" "k_eb_sr_thr uniform_s20_d16 2 4" \
-            "k_rb_sr banded_s20_b8 128 0" "k_eb_sr_lean c3_reddit_like 128 4 c3" \
+            "k_rb_sr uniform_s20_d16 16 0" "k_eb_sr_lean c3_reddit_like 128 4 c3" \
             "k_eb_prep_uniform powerlaw_s20_d16 64 4" "k_rb_sr_tile banded_s20_b8 128 0" \
-            "k_rb_sr_tile_direct banded_s20_b8 16 0"; do
+            "k_rb_sr_tile_direct banded_s20_b8 16 0" "k_rb_cm_rows banded_s20_b8 32 2"; do
   set -- $spec
   wl=${5:-suite}
   case_name="$2/N$3"
