@@ -944,7 +944,7 @@ class _RefArm:
         self.cores = os.cpu_count() or 1
         self.handles, self.dense, self.pairs = {}, [], []
         self.panelled = []
-        self.choice = []
+        self.choice, self.times, self.nnz, self.rm = [], [], [], []
         if self.R is None:
             return
         R = self.R
@@ -971,15 +971,20 @@ class _RefArm:
                 self.dense.append(d_cm)
             del x
             best, best_t = 0, float("inf")
+            times = [None] * 8
             for k in (range(8) if select else (0,)):
                 dk = d_cm if (k >> 1) & 1 else d_rm
                 if dk is None:
                     continue
                 if R.ref_time_spmm_once_f32(h, dk, k, self.cores, 8, 8, C.byref(secs)):
                     raise RuntimeError(R.ref_last_error().decode())
+                times[k] = secs.value
                 if secs.value < best_t:
                     best, best_t = k, secs.value
+            self.times.append(times)
+            self.nnz.append(nnz)
             self.choice.append(best)
+            self.rm.append(d_rm)
             self.pairs.append((h, d_cm if (best >> 1) & 1 else d_rm, best, 2 * nnz * n))
         self.flops = sum(f for *_, f in self.pairs)
 
@@ -992,6 +997,46 @@ class _RefArm:
                 raise RuntimeError(self.R.ref_last_error().decode())
             tot += secs.value
         return tot
+
+    def per_kernel(self):
+        """GFLOP/s of each reference design point over the calls it was timed on (one
+        run per call at P = all host threads; CM points on N <= 16 only)."""
+        out = {}
+        for k in range(8):
+            fl = sum(f for (*_, f), t in zip(self.pairs, self.times) if t[k] is not None)
+            tt = sum(t[k] for t in self.times if t[k] is not None)
+            n = sum(1 for t in self.times if t[k] is not None)
+            if n:
+                out[REF_NAMES[k]] = {"gflops": round(fl / tt / 1e9, 3), "calls": n}
+        return out
+
+    def single_thread(self, max_nnz=3_000_000):
+        """P = 1 on the calls of matrices up to max_nnz (the 2^14- and 2^17-row ones): the
+        chosen design point (one run each) and the serial spmm_reference (the reference's
+        time_kernel_fn, reps 3)."""
+        secs = C.c_double()
+        med, mn, ck = C.c_double(), C.c_double(), C.c_double()
+        fl = t_best = t_ref = 0.0
+        n = 0
+        for (h, d, k, f), nnz in zip(self.pairs, self.nnz):
+            if nnz > max_nnz:
+                continue
+            if self.R.ref_time_spmm_once_f32(h, d, k, 1, 8, 8, C.byref(secs)):
+                raise RuntimeError(self.R.ref_last_error().decode())
+            t_best += secs.value
+            n += 1
+            fl += f
+        # spmm_reference needs its X row-major: the RM operand of each pair
+        for (h, d, k, f), nnz, x_rm in zip(self.pairs, self.nnz, self.rm):
+            if nnz > max_nnz:
+                continue
+            if self.R.ref_time_spmm_dense_reference_f32(h, x_rm, C.byref(secs)):
+                raise RuntimeError(self.R.ref_last_error().decode())
+            t_ref += secs.value
+        if not n:
+            return None
+        return {"calls": n, "best_point_gflops": round(fl / t_best / 1e9, 3),
+                "spmm_reference_gflops": round(fl / t_ref / 1e9, 3) if t_ref else None}
 
     def choices(self):
         out = {}
@@ -1017,6 +1062,8 @@ def _cpu_baseline(mats, ns_override=None, passes=3):
     arm.one_pass()  # warm-up (first touch of X, the pool's threads)
     secs = sorted(arm.one_pass() for _ in range(passes))[passes // 2]
     v = arm.flops / secs / 1e9
+    per_kernel = arm.per_kernel()
+    p1 = arm.single_thread()
     arm.close()
     whole = "every matrix whole" if not arm.panelled else \
         f"{', '.join(arm.panelled)} as a middle row panel of {REF_PANEL_NNZ} nnz"
@@ -1025,7 +1072,18 @@ def _cpu_baseline(mats, ns_override=None, passes=3):
                       f"{len(arm.pairs)} (matrix, N) calls of the workload on its fastest "
                       f"reference design point ({whole}); median of {passes} passes of "
                       f"{secs:.2f} s",
-            "kernels": arm.choices()}
+            "kernels": arm.choices(), "per_kernel_all_threads": per_kernel,
+            "single_thread_s14_s17": p1, "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args):

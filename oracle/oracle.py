@@ -113,6 +113,9 @@ def ref():
         R.ref_time_spmm_once_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
                                              C.c_int64, C.c_int64, C.POINTER(C.c_double)]
         R.ref_time_spmm_once_f32.restype = C.c_int
+        R.ref_time_spmm_dense_reference_f32.argtypes = [C.c_void_p, C.c_void_p,
+                                                        C.POINTER(C.c_double)]
+        R.ref_time_spmm_dense_reference_f32.restype = C.c_int
         R.ref_partition.argtypes = [C.c_void_p, C.c_int, _i64p, _i64p, _i64p]
         R.ref_partition.restype = C.c_int
         R.ref_row_index_of.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]

@@ -242,6 +242,19 @@ int ref_time_spmm_once_f32(void* hp, void* dp, int kernel, int64_t P, int64_t W,
     });
 }
 
+// spmm_reference (spmm.hpp:16-32, serial) timed once on a laid-out X, result dropped.
+int ref_time_spmm_dense_reference_f32(void* hp, void* dp, double* seconds) {
+    auto* h = static_cast<RefCsr*>(hp);
+    const auto& x = *static_cast<const DenseMatrix<float>*>(dp);
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto y = spmm_reference(h->f, x);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (y.data.empty() && x.num_cols > 0 && h->f.num_rows > 0) *seconds = -1.0;
+    });
+}
+
 // partition_elements — partition.hpp:45-64.
 int ref_partition(void* hp, int p, int64_t* begin, int64_t* end, int64_t* row) {
     auto* h = static_cast<RefCsr*>(hp);

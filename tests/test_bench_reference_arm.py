@@ -61,3 +61,18 @@ def test_reference_arm_without_selection_runs_rb_rm_sr():
         assert arm.choices() == {"RB+RM+SR": 6}
     finally:
         arm.close()
+
+
+def test_cpu_baseline_reports_per_kernel_and_single_thread():
+    from oracle import oracle as O
+
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    import bench
+
+    cb = bench._cpu_baseline(_mats(), passes=1)
+    assert cb["value"] > 0 and cb["kind"] == "reference"
+    assert set(cb["per_kernel_all_threads"]) <= set(bench.REF_NAMES)
+    assert cb["per_kernel_all_threads"]["RB+RM+SR"]["calls"] == 6
+    p1 = cb["single_thread_s14_s17"]
+    assert p1["calls"] == 6 and p1["best_point_gflops"] > 0 and p1["spmm_reference_gflops"] > 0
