@@ -27,6 +27,28 @@ tot = sum(b for b, _ in sizes) * 4 / 1e9
 print(f"bytes each way per step: {tot:.3f} GB", flush=True)
 
 
+def run_multi(k, steps=5):
+    """k streams per direction, calls assigned round-robin."""
+    ups = [torch.cuda.Stream() for _ in range(k)]
+    downs = [torch.cuda.Stream() for _ in range(k)]
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(comp)
+    for st in ups + downs:
+        st.wait_stream(comp)
+    for _ in range(steps):
+        for i in range(len(sizes)):
+            with torch.cuda.stream(ups[i % k]):
+                dB[i].copy_(hB[i], non_blocking=True)
+            with torch.cuda.stream(downs[i % k]):
+                hC[i].copy_(dC[i], non_blocking=True)
+    for st in ups + downs:
+        comp.wait_stream(st)
+    e.record(comp)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
 def run(mode, steps=5):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -52,5 +74,5 @@ def run(mode, steps=5):
 
 for mode in ("independent", "transfers_only", "independent", "transfers_only"):
     print(f"{mode:16s} {run(mode):8.2f} ms per step", flush=True)
-# big transfers only (the 2^20-row calls) vs small ones only
-big = [i for i, (b, _) in enumerate(sizes) if b >= (1 << 20) * 2]
+for k in (1, 2, 4, 2, 1):
+    print(f"independent x{k} streams per direction {run_multi(k):8.2f} ms per step", flush=True)
