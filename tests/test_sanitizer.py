@@ -1,4 +1,4 @@
-"""compute-sanitizer memcheck + racecheck over every kernel (8 design points, fast and
+"""compute-sanitizer memcheck, racecheck, synccheck and initcheck over every kernel (8 design points, fast and
 exact, f32 and f64, W 4/32) plus the selector and graph dispatch (tools/sanitize.py)."""
 import os
 import shutil
@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):
     import torch
 
