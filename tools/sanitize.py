@@ -83,6 +83,14 @@ for rl in ("1", "8"):
     sk.spmm_device(0, d, Bw, torch.empty(2000, 36, device="cuda"))
 del os.environ["DASPMM_TILE"], os.environ["DASPMM_TILE_RL"]
 sk.reload_env()
+# RB+CM+SR lanes over rows (forced on every shape): column blocks of 1..8, ragged N
+os.environ["DASPMM_CM_ROWS"] = "2"
+sk.reload_env()
+for n in (1, 3, 8, 13, 64):
+    Bcm = torch.rand(n, 2000, device="cuda")
+    sk.spmm_device(2, d, Bcm, torch.empty(2000, n, device="cuda"))
+del os.environ["DASPMM_CM_ROWS"]
+sk.reload_env()
 # replicated RB+RM+SR epilogue (fused row-panel SpMM + all-gather), three destinations
 for n in (3, 32, 128):
     B = torch.rand(2000, n, device="cuda")
