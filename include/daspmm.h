@@ -241,6 +241,9 @@ int daspmm_selected_cache_info(const daspmm_csr* csr, int64_t* graphs, int64_t* 
  * tree_reduce (reduce.hpp:46-55) and conditional_reduce (reduce.hpp:57-102).
  * Host arrays in, host arrays out. w is a power of two in [1, 32]. */
 int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out);
+/* The reference's std_row (features.hpp:27-35) as one dependent chain of double adds on
+ * the device: the check for the block-wide exact sum daspmm_extract_features uses. */
+int daspmm_debug_std_chain(const daspmm_csr* csr, double* out);
 int daspmm_debug_conditional_scan_f64(const double* values, const int64_t* ids, int64_t w,
                                       double* out);
 

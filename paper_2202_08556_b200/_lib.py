@@ -43,6 +43,7 @@ SIGNATURES = {
     "daspmm_csr_create_panel": (C.c_int, [_vp, _i64, _i64, _vp, C.POINTER(_vp)]),
     "daspmm_csr_destroy": (C.c_int, [_vp]),
     "daspmm_csr_values_updated": (C.c_int, [_vp]),
+    "daspmm_debug_std_chain": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "daspmm_csr_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _ip, _i64p, _i64p]),
     "daspmm_csr_device_arrays": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "daspmm_spmm": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, C.c_int, _i64, _i64, _vp, _i64,

@@ -33,7 +33,7 @@ LIB_SOURCES = ["abi.cu", "features.cu", "select.cu", "graph.cu", "spmm_rb_sr.cu"
                "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu", "spmm_tma.cu",
                "multi.cu", "spmm_pr_wide.cu", "spmm_tile.cu", "spmm_cm.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "dispatch.h", "internal.h", "launch_sr.cuh",
-           "launch_pr.cuh", "lean.cuh", "tma_gather.cuh", "tile.cuh"]
+           "launch_pr.cuh", "lean.cuh", "tma_gather.cuh", "tile.cuh", "exact_sum.cuh"]
 
 
 def _mtime(p):

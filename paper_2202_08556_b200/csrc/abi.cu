@@ -1157,6 +1157,12 @@ int daspmm_plan_info(const daspmm_csr* h, int kernel, int64_t N, const void* B, 
     return DASPMM_OK;
 }
 
+int daspmm_debug_std_chain(const daspmm_csr* h, double* out) {
+    if (!h || !out) return fail(DASPMM_ERR_INVALID_ARG, "debug_std_chain: null argument");
+    if (h->M <= 0) return fail(DASPMM_ERR_INVALID_ARG, "extract_features: matrix has no rows to summarize");
+    return std_chain(h, out);
+}
+
 int daspmm_debug_tree_reduce_f64(const double* values, int64_t w, double* out) {
     if (w < 1 || w > 32 || !is_pow2(w))
         return fail(DASPMM_ERR_INVALID_ARG, "tree_reduce: length must be a power of two <= 32");

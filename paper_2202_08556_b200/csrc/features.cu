@@ -15,6 +15,7 @@
 #include <cmath>
 #include <vector>
 
+#include "exact_sum.cuh"
 #include "internal.h"
 
 namespace daspmm {
@@ -64,27 +65,31 @@ __global__ void k_popcount(const unsigned* __restrict__ bitmap, int64_t words,
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
-// Replays features.hpp:27-35 in the reference's order: the sum is one dependent chain of
-// double adds, so one thread runs it — but out of shared memory: the whole block first
-// computes the next kStdChunk per-row terms q_r = fl(fl(len_r - mean)^2) with coalesced
-// loads (the terms are independent; only their sum is sequential), then thread 0 adds
-// them in row order. The chain costs one __dadd_rn latency per row instead of a global
-// load round trip per row (~19 ns/row before).
+// Replays features.hpp:27-35 in the reference's order with the reference's bits: the
+// whole block runs the binade-wise exact prefix sum (exact_sum.cuh).
 constexpr int kStdThreads = 1024;
-constexpr int kStdChunk = 4 * kStdThreads;  // 32 KB of staged terms
 
-__global__ void __launch_bounds__(kStdThreads) k_std_sequential(const int* __restrict__ rp, int M,
-                                                                DevFeatures* f) {
-    __shared__ double q[kStdChunk];
-    const double mean = f->mean;
+__global__ void __launch_bounds__(kStdThreads) k_std_exact(const int* __restrict__ rp, int M,
+                                                           DevFeatures* f) {
+    const double ss = exact_sequential_sum<kStdThreads>(rp, M, f->mean);
+    if (threadIdx.x == 0) {
+        f->std_exact = __dsqrt_rn(__ddiv_rn(ss, double(M)));
+        f->exact_valid = 1;
+    }
+}
+
+// The same sum as one dependent chain of double adds (the reference's loop verbatim, one
+// thread, terms staged by the block): the check the block sum is tested against
+// (daspmm_debug_std_chain).
+constexpr int kChainChunk = 4 * kStdThreads;
+
+__global__ void __launch_bounds__(kStdThreads) k_std_chain(const int* __restrict__ rp, int M,
+                                                           double mean, double* out) {
+    __shared__ double q[kChainChunk];
     double ss = 0.0;
-    for (int base = 0; base < M; base += kStdChunk) {
-        const int n = min(kStdChunk, M - base);
-        for (int i = threadIdx.x; i < n; i += kStdThreads) {
-            const int r = base + i;
-            const double d = __dsub_rn(double(__ldg(rp + r + 1) - __ldg(rp + r)), mean);
-            q[i] = __dmul_rn(d, d);
-        }
+    for (int base = 0; base < M; base += kChainChunk) {
+        const int n = min(kChainChunk, M - base);
+        for (int i = threadIdx.x; i < n; i += kStdThreads) q[i] = std_term(rp, base + i, mean);
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll 16
@@ -92,10 +97,7 @@ __global__ void __launch_bounds__(kStdThreads) k_std_sequential(const int* __res
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        f->std_exact = __dsqrt_rn(__ddiv_rn(ss, double(M)));
-        f->exact_valid = 1;
-    }
+    if (threadIdx.x == 0) *out = __dsqrt_rn(__ddiv_rn(ss, double(M)));
 }
 
 // One warp per row writes the row's id into its nonzeros' slots (COO expansion).
@@ -398,13 +400,26 @@ int exact_std(daspmm_csr* h, double* out) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->h_feat.exact_valid) {
         DeviceGuard g(h->device);
-        k_std_sequential<<<1, kStdThreads>>>(h->rp, int(h->M), h->d_feat);
+        k_std_exact<<<1, kStdThreads>>>(h->rp, int(h->M), h->d_feat);
         cudaError_t e = cudaMemcpy(&h->h_feat, h->d_feat, sizeof(DevFeatures),
                                    cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(e, "exact std");
     }
     *out = h->h_feat.std_exact;
     return DASPMM_OK;
+}
+
+int std_chain(const daspmm_csr* h, double* out) {
+    DeviceGuard g(h->device);
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double));
+    if (e == cudaSuccess) {
+        k_std_chain<<<1, kStdThreads>>>(h->rp, int(h->M), h->h_feat.mean, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "std_chain");
 }
 
 }  // namespace daspmm

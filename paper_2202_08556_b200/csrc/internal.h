@@ -96,6 +96,8 @@ int compute_features(daspmm_csr* h, cudaStream_t s);
 // Builds h->coo_rows once (never call inside a stream capture).
 int ensure_coo(const daspmm_csr* h, cudaStream_t s);
 int exact_std(daspmm_csr* h, double* out);
+// The reference's std_row as one dependent add chain (test hook for the block sum).
+int std_chain(const daspmm_csr* h, double* out);
 // Examines / builds h's dense row-panel tiles once (never call inside a stream capture).
 int ensure_tiles(const daspmm_csr* h, cudaStream_t s);
 // Implemented in abi.cu

@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "exact_sum.cuh"
 #include "internal.h"
 
 namespace daspmm {
@@ -330,24 +331,19 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
         __syncthreads();
         if (!ambiguous) break;
         // Rare: a std_row threshold inside the proven interval. Replay the
-        // reference's sequential sum once (features.hpp:27-35) and cache it.
-        if (threadIdx.x == 0) {
-            const double mean = feat->mean;
-            double ss = 0.0;
+        // reference's sequential sum once (features.hpp:27-35, the block-wide exact sum
+        // of exact_sum.cuh) and cache it.
+        {
             const int M = int(feat->rows);
-            int prev = rp[0];
-            for (int r = 0; r < M; ++r) {
-                const int next = rp[r + 1];
-                const double d = __dsub_rn(double(next - prev), mean);
-                ss = __dadd_rn(ss, __dmul_rn(d, d));
-                prev = next;
+            const double ss = M > 0 ? exact_sequential_sum<kSelThreads>(rp, M, feat->mean) : 0.0;
+            if (threadIdx.x == 0) {
+                const double sd = M > 0 ? __dsqrt_rn(__ddiv_rn(ss, double(M))) : 0.0;
+                feat->std_exact = sd;
+                feat->exact_valid = 1;
+                s_exact = sd;
+                s_have = 1;
+                ambiguous = 0;
             }
-            const double sd = M > 0 ? __dsqrt_rn(__ddiv_rn(ss, double(M))) : 0.0;
-            feat->std_exact = sd;
-            feat->exact_valid = 1;
-            s_exact = sd;
-            s_have = 1;
-            ambiguous = 0;
         }
         __syncthreads();
     }

@@ -790,3 +790,57 @@ def test_pr_group_width_above_a_warp(sk, W):
     with pytest.raises(RuntimeError, match="supports 2..1024"):
         sk.spmm(sk.KernelId.from_index(1), cases[0], sk.DenseMatrix.zeros(2100, 2),
                 sk.WorkerConfig(1, 2048, 2))
+
+
+@pytest.mark.parametrize("case", ["uniform_small", "uniform_chunk_edges", "dyadic_mean",
+                                  "all_equal", "leading_equal_then_skew", "powerlaw_huge_rows",
+                                  "one_huge_row", "tiny_and_huge_mix", "large_2p20"])
+def test_exact_std_block_sum_matches_sequential(sk, case):
+    """extract_features' std_row comes from the block-wide binade prefix sum
+    (csrc/exact_sum.cuh); it must equal, bit for bit, the reference's loop run as one
+    dependent chain of double adds (daspmm_debug_std_chain) and the C oracle."""
+    import ctypes as C
+
+    from paper_2202_08556_b200 import _lib
+
+    rng = np.random.default_rng(hash(case) % (1 << 31))
+    if case == "uniform_small":
+        mats = [rng.integers(0, 40, m) for m in (1, 2, 3, 7, 33, 1000, 5001)]
+    elif case == "uniform_chunk_edges":  # around the 8192-term chunk of a 1024-thread block
+        mats = [rng.integers(0, 40, m) for m in (8191, 8192, 8193, 16384, 16385, 24577)]
+    elif case == "dyadic_mean":  # mean = 16 exactly: integer terms, no rounding for long
+        mats = [np.resize(np.array([10, 22, 16, 16]), m) for m in (4096, 100000)]
+        mats.append(rng.permutation(np.resize(np.arange(0, 33), 33 * 3000)))
+    elif case == "all_equal":  # every term 0: the sum stays +0 (std 0)
+        mats = [np.full(m, 9) for m in (1, 10, 70000)]
+    elif case == "leading_equal_then_skew":
+        mats = [np.concatenate([np.full(50000, 5), rng.integers(0, 3000, 30000)])]
+    elif case == "powerlaw_huge_rows":
+        w = 1.0 / np.arange(1, 200001) ** 1.5
+        mats = [rng.multinomial(3_000_000, w / w.sum())]
+    elif case == "one_huge_row":
+        v = np.zeros(100000, np.int64)
+        v[777] = 2_000_000
+        mats = [v, np.roll(v, 50000)]
+    elif case == "tiny_and_huge_mix":
+        v = rng.integers(0, 3, 300000)
+        v[rng.integers(0, 300000, 50)] = rng.integers(100000, 400000, 50)
+        mats = [v]
+    else:
+        mats = [rng.integers(0, 33, 1 << 20)]
+    for lens in mats:
+        lens = np.asarray(lens, np.int64)
+        M = lens.size
+        rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        nnz = int(rp[-1])
+        ci = np.zeros(nnz, np.int64)
+        a = sk.CsrMatrix(M, 1, rp, ci, np.ones(nnz, np.float32), np.float32)
+        d = sk.DeviceCsr.from_host(a)
+        got = sk.extract_features(d, 8).std_row
+        chain = C.c_double()
+        _lib.check(sk.lib().daspmm_debug_std_chain(d._h, C.byref(chain)))
+        assert got == chain.value, (case, M, got, chain.value)
+        if nnz <= 4_000_000:
+            want = O.extract_features(O.Csr(M, 1, rp, ci, np.ones(nnz)))[2]
+            assert got == want, (case, M, got, want)
+        d.close()
