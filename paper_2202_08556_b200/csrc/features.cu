@@ -46,21 +46,25 @@ k_row_terms(const int* __restrict__ rp, int M, double mean, double* __restrict__
     if (threadIdx.x == 0) partial[blockIdx.x] = sm[0];
 }
 
+// Distinct columns touched (K_touched): a byte per column set to 1 by every nonzero that
+// finds it still 0 (a check before the store keeps hot power-law columns from becoming a
+// stream of same-address writes; the race only ever writes 1), then the 1-bytes counted a
+// word at a time (each byte is 0x00 or 0x01, so popc of the word counts them).
 __global__ void k_cols_touched(const int* __restrict__ ci, int64_t nnz,
-                               unsigned* __restrict__ bitmap) {
+                               unsigned char* marks) {
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int c = __ldg(ci + e);
-        atomicOr(bitmap + (c >> 5), 1u << (c & 31));
+        if (marks[c] == 0) marks[c] = 1;  // a stale 0 only repeats the store
     }
 }
 
-__global__ void k_popcount(const unsigned* __restrict__ bitmap, int64_t words,
+__global__ void k_popcount(const unsigned* __restrict__ words_in, int64_t words,
                            unsigned long long* __restrict__ out) {
     unsigned long long acc = 0;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
          i += int64_t(gridDim.x) * blockDim.x)
-        acc += __popc(bitmap[i]);
+        acc += __popc(words_in[i]);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
@@ -331,7 +335,7 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
     if (blocks < 1) blocks = 1;
     double* partial = nullptr;
     unsigned long long* counters = nullptr;  // [0] empty rows, [1] cols touched
-    const int64_t words = (h->K + 31) / 32;
+    const int64_t words = (h->K + 3) / 4;  // one byte per column, counted per 32-bit word
     unsigned* bitmap = nullptr;
     if ((e = cudaMalloc(&partial, sizeof(double) * blocks)) != cudaSuccess)
         return cuda_fail(e, "cudaMalloc");
@@ -348,7 +352,7 @@ int compute_features(daspmm_csr* h, cudaStream_t s) {
                                                      counters);
     if (h->nnz > 0) {
         const int b2 = int(std::min<int64_t>((h->nnz + 255) / 256, 148 * 16));
-        k_cols_touched<<<b2, 256, 0, s>>>(h->ci, h->nnz, bitmap);
+        k_cols_touched<<<b2, 256, 0, s>>>(h->ci, h->nnz, reinterpret_cast<unsigned char*>(bitmap));
         const int b3 = int(std::min<int64_t>((words + 255) / 256, 148 * 4));
         k_popcount<<<std::max(b3, 1), 256, 0, s>>>(bitmap, words, counters + 1);
     }
