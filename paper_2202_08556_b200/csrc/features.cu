@@ -161,6 +161,38 @@ __global__ void k_tile_spans(const int* __restrict__ rp, const int* __restrict__
     }
 }
 
+// Load-balanced forms of the two checks above, used once the COO row ids exist (they do
+// whenever a fast RB+RM+SR call asks for tiles): rows are column-sorted iff no nonzero is
+// followed, inside its row, by a column <= its own (one thread per nonzero); then a
+// panel's window is [min first column, max last column] of its rows (one thread per
+// panel, two loads per row). The warp-per-panel scan above takes as long as the longest
+// panel, i.e. ~1.5 ms on a power-law 2^20-row matrix that can never be tiled.
+__global__ void k_rows_unsorted(const int* __restrict__ ci, const int* __restrict__ rows,
+                                int64_t nnz, int* __restrict__ unsorted) {
+    bool bad = false;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e + 1 < nnz;
+         e += int64_t(gridDim.x) * blockDim.x)
+        bad |= __ldg(rows + e + 1) == __ldg(rows + e) && __ldg(ci + e + 1) <= __ldg(ci + e);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *unsorted = 1;
+}
+
+__global__ void k_tile_windows(const int* __restrict__ rp, const int* __restrict__ ci, int M,
+                               int64_t n_pan, int* __restrict__ width, int* __restrict__ c0) {
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n_pan) return;
+    const int r0 = int(p * kPanelRows), r1 = min(M, r0 + kPanelRows);
+    int lo = INT_MAX, hi = -1;
+    for (int r = r0; r < r1; ++r) {
+        const int s = __ldg(rp + r), e = __ldg(rp + r + 1);
+        if (s < e) {
+            lo = min(lo, __ldg(ci + s));
+            hi = max(hi, __ldg(ci + e - 1));
+        }
+    }
+    width[p] = hi >= lo ? hi - lo + 1 : 0;
+    c0[p] = hi >= lo ? lo : 0;
+}
+
 // One warp per panel: zero its tile, then place every nonzero at (col - c0, row - r0).
 __global__ void k_tile_fill(const int* __restrict__ rp, const int* __restrict__ ci,
                             const float* __restrict__ va, int M, int64_t n_pan,
@@ -207,7 +239,13 @@ int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaMalloc(&h->tile_c0, sizeof(int) * size_t(n_pan));
     if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(int));
     if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, sizeof(int), s);
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && h->coo_rows != nullptr) {
+        const unsigned b1 = unsigned(std::min<int64_t>((h->nnz + 255) / 256, 148 * 16));
+        k_rows_unsorted<<<std::max(b1, 1u), 256, 0, s>>>(h->ci, h->coo_rows, h->nnz, d_bad);
+        k_tile_windows<<<unsigned((n_pan + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M), n_pan,
+                                                                    d_w, h->tile_c0);
+        e = cudaGetLastError();
+    } else if (e == cudaSuccess) {
         const int64_t threads = n_pan * 32;
         k_tile_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M), n_pan,
                                                                     d_w, h->tile_c0, d_bad);
@@ -260,26 +298,55 @@ int ensure_tiles(const daspmm_csr* hc, cudaStream_t s) {
     return DASPMM_OK;
 }
 
-// Column window of every 32-row fine panel: one warp per panel, [min, max] column
-// ({INT_MAX, -1} when the panel holds no nonzero).
+// Column window of every 32-row fine panel, [min, max] column ({INT_MAX, -1} when the
+// panel holds no nonzero). Load-balanced over nonzeros: a thread takes 64 consecutive
+// nonzeros, finds the row of the first by binary search in row_offsets, walks them
+// tracking the row (and so the panel), and merges each panel's run into spans[] with
+// atomicMin / atomicMax — one warp per panel took as long as the densest panel (a
+// power-law 2^20-row matrix: ~0.75 ms for one 100K-nonzero row).
+constexpr int kSpanChunk = 64;
+
+__global__ void k_spans_init(int64_t n_fine, int2* __restrict__ spans) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n_fine;
+         p += int64_t(gridDim.x) * blockDim.x)
+        spans[p] = make_int2(INT_MAX, -1);
+}
+
 __global__ void k_fine_spans(const int* __restrict__ rp, const int* __restrict__ ci, int M,
-                             int64_t n_fine, int2* __restrict__ spans) {
-    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (p >= n_fine) return;
-    const int r0 = int(p * 32), r1 = min(M, r0 + 32);
-    const int s = __ldg(rp + r0), e = __ldg(rp + r1);
+                             int64_t nnz, int2* spans) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t e0 = t * kSpanChunk;
+    if (e0 >= nnz) return;
+    const int64_t e1 = min(nnz, e0 + kSpanChunk);
+    // row holding e0: the last r with rp[r] <= e0 (upper_bound - 1)
+    int lo_r = 0, hi_r = M;  // answer in [lo_r, hi_r)
+    while (hi_r - lo_r > 1) {
+        const int mid = (lo_r + hi_r) >> 1;
+        if (__ldg(rp + mid) <= e0) lo_r = mid;
+        else hi_r = mid;
+    }
+    int r = lo_r;
+    int row_end = __ldg(rp + r + 1);
+    int panel = r >> 5;
     int lo = INT_MAX, hi = -1;
-    for (int i = s + lane; i < e; i += 32) {
-        const int c = __ldg(ci + i);
+    for (int64_t e = e0; e < e1; ++e) {
+        while (e >= row_end) {  // next non-empty row
+            ++r;
+            row_end = __ldg(rp + r + 1);
+        }
+        if ((r >> 5) != panel) {
+            atomicMin(&spans[panel].x, lo);
+            atomicMax(&spans[panel].y, hi);
+            panel = r >> 5;
+            lo = INT_MAX;
+            hi = -1;
+        }
+        const int c = __ldg(ci + e);
         lo = min(lo, c);
         hi = max(hi, c);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) spans[p] = make_int2(lo, hi);
+    atomicMin(&spans[panel].x, lo);
+    atomicMax(&spans[panel].y, hi);
 }
 
 // Fine-panel windows on the device plus, per panel height R = 32 << i, the widest and
@@ -289,9 +356,13 @@ static int compute_spans(daspmm_csr* h, cudaStream_t s) {
     if (h->n_fine == 0) return DASPMM_OK;
     cudaError_t e = cudaMalloc(&h->spans, sizeof(int2) * size_t(h->n_fine));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(spans)");
-    const int64_t threads = h->n_fine * 32;
-    k_fine_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M),
-                                                                 h->n_fine, h->spans);
+    k_spans_init<<<unsigned(std::min<int64_t>((h->n_fine + 255) / 256, 148 * 8)), 256, 0, s>>>(
+        h->n_fine, h->spans);
+    if (h->nnz > 0) {
+        const int64_t threads = (h->nnz + kSpanChunk - 1) / kSpanChunk;
+        k_fine_spans<<<unsigned((threads + 255) / 256), 256, 0, s>>>(h->rp, h->ci, int(h->M),
+                                                                     h->nnz, h->spans);
+    }
     std::vector<int2> hs(size_t(h->n_fine));
     if ((e = cudaGetLastError()) == cudaSuccess)
         e = cudaMemcpyAsync(hs.data(), h->spans, sizeof(int2) * hs.size(), cudaMemcpyDeviceToHost, s);
