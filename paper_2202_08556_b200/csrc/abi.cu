@@ -473,7 +473,9 @@ Plan plan_spmm(const daspmm_csr* h, int kernel, int64_t P, int64_t W, int64_t N,
             if (cl <= 4 && h->n_pan * cl * rl < 65536) rl = 8;
             if (kn.tile_rl == 1 || (kn.tile_rl == 8 && cl <= 4)) rl = kn.tile_rl;  // tuning
             const int64_t thr = h->n_pan * cl * rl;
-            if (thr >= 65536 || kn.tile_force) {
+            // a lane per row (rl = 8) needs twice the threads: banded s14 N = 4 at V = 1
+            // (65536 threads) ran 10.2 us on tiles vs 8.3 on the base walk
+            if (thr >= (rl == 8 ? 131072 : 65536) || kn.tile_force) {
                 p.tile = true;
                 p.lean = false;
                 p.X = 1;
