@@ -720,6 +720,10 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
         "roofline": {"bound": "hbm", "achieved": round(dom_ach, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(dom_ach / peak, 4), "traffic": traffic,
                      "peak_source": peak_kind,
+                     # the DRAM bytes ncu measures for this call (profiles/ncu_traffic.json)
+                     # moved in its measured time, as a fraction of the same peak
+                     "traffic_frac": (round(traffic / (per_call_ms[dom] * 1e-3) / 1e9 / peak, 4)
+                                      if traffic else None),
                      "scope": "dominant call (longest of the step): its algorithmic bytes "
                               "(4(M+1)+8nnz+4N*K_touched+4NM) / its mean CUDA-event time",
                      "dominant": {"call": _key(calls[dom]),
