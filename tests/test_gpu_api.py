@@ -271,3 +271,48 @@ def test_spmm_batch_branches_keep_same_output_order(env):
             y64 = O.spmm_reference(H.to_oracle(m), x64)
             err = np.abs(y.cpu().numpy().astype(np.float64) - y64)
             assert (err <= H.gamma_bound(m, x64, np.float32)).all()
+
+
+def test_concurrent_host_threads_share_a_handle(env):
+    """Four host threads (ctypes releases the GIL, so the library runs them concurrently)
+    call DA-SpMM and plain spmm on one fresh handle, each on its own stream and N: the lazy
+    per-handle builds (COO row ids, row-panel tiles), the decision table and the graph
+    cache must stay consistent; every result holds the gamma bound."""
+    import threading
+
+    torch, gen, sk, model = env
+    M, K, rp, ci, va = gen.banded(1 << 16, 8, seed=5)
+    d = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+    a = sk.CsrMatrix(M, K, rp.cpu().numpy().astype(np.int64), ci.cpu().numpy().astype(np.int64),
+                     va.cpu().numpy(), np.float32)
+    errors = []
+    outs = {}
+
+    def worker(tid):
+        try:
+            n = (4, 16, 32, 128)[tid]
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                B = torch.rand(K, n, device="cuda") - 0.5
+                C1 = torch.empty(M, n, device="cuda")
+                C2 = torch.empty(M, n, device="cuda")
+                for _ in range(20):
+                    sk.spmm_selected(d, model, B, C1, stream=stream)
+                    sk.spmm_device(0, d, B, C2, stream=stream)
+            stream.synchronize()
+            outs[tid] = (B.cpu().numpy(), C1.cpu().numpy(), C2.cpu().numpy())
+        except Exception as ex:  # surfaced below
+            errors.append(repr(ex))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for tid, (x, y1, y2) in outs.items():
+        x64 = x.astype(np.float64)
+        y64 = O.spmm_reference(H.to_oracle(a), x64)
+        bound = H.gamma_bound(a, x64, np.float32)
+        assert (np.abs(y1 - y64) <= bound).all(), tid
+        assert (np.abs(y2 - y64) <= bound).all(), tid
