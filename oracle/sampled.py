@@ -47,13 +47,16 @@ def sample_rows(rp_host: np.ndarray, n_random: int = 384, seed: int = 0,
     return rows.astype(np.int64)
 
 
-def check(rp, ci, va, K, B, Cout, rows, cols=None, b_colmajor=False, dtype=None, row0=0):
+def check(rp, ci, va, K, B, Cout, rows, cols=None, b_colmajor=False, dtype=None, row0=0,
+          exact=False):
     """Check rows x cols of Cout (device M x N row-major) = A @ B on the sampled entries.
     ``row0``: Cout holds rows [row0, ...) of A only (a row panel's output).
 
     rp/ci/va: device CSR tensors (int32/int64 offsets and columns); B: device tensor,
     K x N row-major, or the N x K buffer of a column-major B when b_colmajor. Returns a
-    dict with rows/cols checked, worst err/bound ratio and ok."""
+    dict with rows/cols checked, worst err/bound ratio and ok. ``exact``: ok only if
+    every sampled entry equals spmm_reference's (fp64 sequential sum) bit for bit — the
+    bar for the RB+SR kernels in exact mode on fp64 operands."""
     import torch
 
     dev = rp.device
@@ -104,4 +107,6 @@ def check(rp, ci, va, K, B, Cout, rows, cols=None, b_colmajor=False, dtype=None,
     ratio = float((err / bound).max()) if err.size else 0.0
     return {"rows": int(len(rows)), "cols": int(y.shape[1]), "nnz": total,
             "max_ratio": ratio, "max_abs_err": float(err.max()) if err.size else 0.0,
-            "nan": bool(np.isnan(y).any()), "ok": bool((err <= bound).all()) and not np.isnan(y).any()}
+            "nan": bool(np.isnan(y).any()),
+            "ok": (bool(np.array_equal(y, y64)) if exact
+                   else bool((err <= bound).all()) and not np.isnan(y).any())}

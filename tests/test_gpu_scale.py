@@ -242,3 +242,25 @@ def test_c5_row_and_column_sampled(env):
     del B, C
     _MATS.clear()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["uniform_s17_d16", "powerlaw_s17_d16", "banded_s17_b8"])
+def test_fp64_exact_mode_bit_identical_at_scale(env, name):
+    """fp64 (the reference's double-precision path) in exact mode at a suite scale: RB+RM+SR
+    and RB+CM+SR equal spmm_reference<double> bit for bit on sampled rows (rows are
+    independent, so a sampled row is the full row's sum, in the reference's order)."""
+    torch, gen, sk, _ = env
+    mk = dict((n, m) for n, m, _ in gen.workload("suite", dtype=torch.float64))[name]
+    M, K, rp, ci, va = mk()
+    d = sk.DeviceCsr.from_device(M, K, rp, ci, va)
+    rows = S.sample_rows(rp.cpu().numpy().astype(np.int64), seed=3)
+    for n in (8, 33):
+        B = gen.dense_operand(K, n, seed=60 + n, dtype=torch.float64)
+        for kid in (0, 2):
+            cm = (kid >> 1) & 1
+            Bop = B.t().contiguous() if cm else B
+            C = torch.full((M, n), float("nan"), dtype=torch.float64, device="cuda")
+            sk.spmm_device(kid, d, Bop, C, exact=True)
+            torch.cuda.synchronize()
+            res = S.check(rp, ci, va, K, Bop, C, rows, b_colmajor=bool(cm), exact=True)
+            assert res["ok"], (name, n, kid, res)
