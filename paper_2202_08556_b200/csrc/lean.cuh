@@ -14,8 +14,9 @@
 //     segment end), or a contiguous nonzero range in 8-element blocks with the COO row
 //     ids loaded as quads too (range walk): a block that stays inside the current row
 //     runs branch-free; masked slots (range edges) issue no load and no FFMA;
-//   * two quads per iteration: 8 independent B-row gathers in flight per lane before
-//     the 32 FFMAs that consume them.
+//   * the segment walks take two quads per iteration (8 independent B-row gathers in
+//     flight per lane before the FFMAs that consume them); the range walk takes one and
+//     spends the registers on occupancy instead (measured, below).
 //
 //   RB (K0, opt-in DASPMM_LEAN_RB=1): group owns rows [g*rpg, (g+1)*rpg), one segment
 //            per row, every row stored (empty rows store zeros).
@@ -40,7 +41,16 @@ namespace daspmm {
 // (64 registers, 32 warps: uniform s20 N = 128 1294 -> 1245 us), the EB walks lose at 4
 // (power-law N = 16 range walk 217 -> 303 us) and keep 3 (80 registers).
 constexpr int kLeanMinBlocksRB = 4;
+// Range walk: one quad of (col, val, row) per iteration and 4 CTAs per SM for groups of
+// >= 4 lanes (56 registers), 3 below (68). Two quads per iteration (8 gathers in flight,
+// 80 registers) ran power-law s20 N = 8 151.9 -> 137.7 us and N = 16 194.8 -> 168.2 us
+// slower (profiles/r02_rw_quads_probe.txt): occupancy beats per-lane depth here.
+#ifndef DASPMM_RW_QUADS
+#define DASPMM_RW_QUADS 1
+#endif
 constexpr int kLeanMinBlocksEB = 3;
+template <int LPR>
+constexpr int lean_rw_min_blocks() { return LPR >= 4 ? 4 : 3; }
 
 struct Quad {
     int c[4];
@@ -158,20 +168,21 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
 #pragma unroll
         for (int i = 0; i < V; ++i) acc.v[i] = 0.f;
     };
-    for (int q = e0 & ~3; q < e1; q += 8) {
-        const int lo = max(e0 - q, 0), hi = min(e1 - q, 8);  // valid slots [lo, hi)
+    constexpr int BLK = 4 * DASPMM_RW_QUADS;  // elements per iteration (1 or 2 quads)
+    for (int q = e0 & ~3; q < e1; q += BLK) {
+        const int lo = max(e0 - q, 0), hi = min(e1 - q, BLK);  // valid slots [lo, hi)
         const unsigned valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
         const Quad A0 = load_quad(a, q, nnz);
         const int4 R0 = load_rquad(a, q, nnz);
         Quad A1;  // slots 4..7 are valid only when loaded
         int4 R1 = R0;
-        if (hi > 4) {  // group-uniform
+        if (BLK > 4 && hi > 4) {  // group-uniform
             A1 = load_quad(a, q + 4, nnz);
             R1 = load_rquad(a, q + 4, nnz);
         }
-        Frag<float, V> b[8];
+        Frag<float, V> b[BLK];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < BLK; ++j) {
             const int c = j < 4 ? A0.c[j] : A1.c[j - 4];
             if (colok && (valid & (1u << j)))
                 b[j] = ld_frag<float, V>(reinterpret_cast<const float*>(
@@ -180,7 +191,7 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
         const int rlast = hi > 4 ? quad_get(R1, hi - 5) : quad_get(R0, hi - 1);
         if (rlast == r) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < BLK; ++j) {
                 const float v = j < 4 ? A0.v[j] : A1.v[j - 4];
                 if (valid & (1u << j)) {
 #pragma unroll
@@ -189,7 +200,7 @@ __device__ __forceinline__ void range_walk(const SpmmArgs<float>& a, const int e
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < BLK; ++j) {
                 const float v = j < 4 ? A0.v[j] : A1.v[j - 4];
                 const int rid = j < 4 ? quad_get(R0, j) : quad_get(R1, j - 4);
                 if (valid & (1u << j)) {
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_s
 // EB, range walk: the chunk as one nonzero range with COO row ids (range_walk). Suits
 // short rows (power-law tails), where per-segment row-offset lookups would dominate.
 template <int V, int LPR, int NT = kThreads>
-__global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
+__global__ void __launch_bounds__(NT, lean_rw_min_blocks<LPR>() * (kThreads / NT)) k_eb_sr_lean_rw(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
