@@ -40,7 +40,10 @@ namespace daspmm {
 // / (256 x minB); scaled for smaller CTAs). Measured on B200: the RB walk gains from 4
 // (64 registers, 32 warps: uniform s20 N = 128 1294 -> 1245 us), the EB walks lose at 4
 // (power-law N = 16 range walk 217 -> 303 us) and keep 3 (80 registers).
-constexpr int kLeanMinBlocksRB = 4;
+#ifndef DASPMM_RBL_MINB
+#define DASPMM_RBL_MINB 4
+#endif
+constexpr int kLeanMinBlocksRB = DASPMM_RBL_MINB;
 // Range walk: one quad of (col, val, row) per iteration and 4 CTAs per SM for groups of
 // >= 4 lanes (56 registers), 3 below (68). Two quads per iteration (8 gathers in flight,
 // 80 registers) ran power-law s20 N = 8 151.9 -> 137.7 us and N = 16 194.8 -> 168.2 us
@@ -48,7 +51,17 @@ constexpr int kLeanMinBlocksRB = 4;
 #ifndef DASPMM_RW_QUADS
 #define DASPMM_RW_QUADS 1
 #endif
+// EB segment walk (long rows, e.g. c3): wide groups (>= 16 lanes) take one quad per
+// iteration at 5 CTAs per SM (48 registers): c3 3.66 -> 3.29 ms; narrower groups keep two
+// quads at 3 (profiles/r02_seg_quads_probe.txt).
 constexpr int kLeanMinBlocksEB = 3;
+template <int LPR>
+constexpr int lean_seg_min_blocks() { return LPR >= 16 ? 5 : kLeanMinBlocksEB; }
+template <int LPR>
+constexpr int lean_seg_quads() { return LPR >= 16 ? 1 : 2; }
+#ifndef DASPMM_RBL_QUADS
+#define DASPMM_RBL_QUADS 2
+#endif
 template <int LPR>
 constexpr int lean_rw_min_blocks() { return LPR >= 4 ? 4 : 3; }
 
@@ -86,30 +99,31 @@ __device__ __forceinline__ Quad load_quad(const SpmmArgs<float>& a, int q, int n
 // Bc = &B[0][col] as bytes, ldb_bytes = ldb * sizeof(float): each gather address is one
 // IMAD.WIDE (col index x row pitch + base). Masked slots (outside [s, e1)) issue no load
 // and no FFMA (predicated), so stale registers never reach the accumulator.
-template <int V>
+template <int V, int QB = 2>
 __device__ __forceinline__ Frag<float, V> row_segment(const SpmmArgs<float>& a, int s, int e1,
                                                       const char* __restrict__ Bc,
                                                       int ldb_bytes, bool colok) {
+    constexpr int BLK = 4 * QB;  // elements per iteration (QB quads)
     Frag<float, V> acc;
 #pragma unroll
     for (int i = 0; i < V; ++i) acc.v[i] = 0.f;
     const int nnz = int(a.nnz);
-    for (int q = s & ~3; q < e1; q += 8) {
-        const int lo = max(s - q, 0), hi = min(e1 - q, 8);  // valid slots [lo, hi)
+    for (int q = s & ~3; q < e1; q += BLK) {
+        const int lo = max(s - q, 0), hi = min(e1 - q, BLK);  // valid slots [lo, hi)
         const unsigned valid = colok ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
         const Quad A0 = load_quad(a, q, nnz);
         Quad A1;  // slots 4..7 are valid only when it is loaded
-        if (hi > 4) A1 = load_quad(a, q + 4, nnz);  // group-uniform
-        Frag<float, V> b[8];
+        if (BLK > 4 && hi > 4) A1 = load_quad(a, q + 4, nnz);  // group-uniform
+        Frag<float, V> b[BLK];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < BLK; ++j) {
             const int c = j < 4 ? A0.c[j] : A1.c[j - 4];
             if (valid & (1u << j))
                 b[j] = ld_frag<float, V>(reinterpret_cast<const float*>(
                     Bc + int64_t(c) * ldb_bytes));
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < BLK; ++j) {
             const float v = j < 4 ? A0.v[j] : A1.v[j - 4];
             if (valid & (1u << j)) {
 #pragma unroll
@@ -233,7 +247,7 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksRB * (kThreads / NT)) k_rb_s
     int s = __ldg(a.rp + r0);
     for (int r = int(r0); r < r1; ++r) {
         const int e1 = __ldg(a.rp + r + 1);
-        const Frag<float, V> acc = row_segment<V>(a, s, e1, Bc, ldb_bytes, colok);
+        const Frag<float, V> acc = row_segment<V, DASPMM_RBL_QUADS>(a, s, e1, Bc, ldb_bytes, colok);
         if (colok) st_frag(a.C + int64_t(r) * a.ldc + col, acc);
         s = e1;
     }
@@ -243,7 +257,7 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksRB * (kThreads / NT)) k_rb_s
 // segment at a time (next row from the COO id of the segment's end, so empty rows cost
 // nothing). Rows cut by the chunk ends take atomics. Suits long rows.
 template <int V, int LPR, int NT = kThreads>
-__global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_sr_lean(const SpmmArgs<float> a) {
+__global__ void __launch_bounds__(NT, lean_seg_min_blocks<LPR>() * (kThreads / NT)) k_eb_sr_lean(const SpmmArgs<float> a) {
     const int gl = threadIdx.x & (LPR - 1);
     const int64_t w = (int64_t(blockIdx.x) * NT + threadIdx.x) / LPR;
     const int64_t e0l = w * a.sub;
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__(NT, kLeanMinBlocksEB * (kThreads / NT)) k_eb_s
         const int rs = __ldg(a.rp + r);
         const int re = __ldg(a.rp + r + 1);
         const int se = min(re, e1);
-        const Frag<float, V> acc = row_segment<V>(a, s, se, Bc, ldb_bytes, colok);
+        const Frag<float, V> acc = row_segment<V, lean_seg_quads<LPR>()>(a, s, se, Bc, ldb_bytes, colok);
         if (colok) {
             float* y = a.C + int64_t(r) * a.ldc + col;
             if (rs >= e0 && re <= e1) {
