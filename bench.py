@@ -117,8 +117,25 @@ def _key(c):
 def _flush(buf):
     """Evicts L2 between timed calls with a READ sweep of a buffer twice the L2 size:
     the lines it leaves are clean, so the next call pays no write-back for them (a
-    zero-fill would leave up to 126 MB of dirty lines for the timed call to drain)."""
+    zero-fill would leave up to 126 MB of dirty lines for the timed call to drain).
+    Then holds the GPU busy (_hold) so the timed call is enqueued before it can start."""
     buf.sum()
+    _hold()
+
+
+HOLD_CYCLES = 200_000  # ~100 us at 1965 MHz
+
+
+def _hold():
+    """A ~100 us device spin on the launching stream before a timed call's start event,
+    so the host's per-call work (operand checks, ctypes, event records) can never land
+    inside the event pair on an idle GPU. Measured (tools/experiments/small_call_probe.py,
+    profiles/r02e_small_call_probe.txt): the per-call times are the same with and without
+    it apart from the first call of a handle, so it is a guard, not a correction. The
+    spin touches no memory, so the flushed L2 state is unchanged."""
+    import torch
+
+    torch.cuda._sleep(HOLD_CYCLES)
 
 
 def _max_over_ranks(v: float, dev) -> float:
@@ -435,6 +452,7 @@ def _warm(calls, one, stream, world, dev, total_flops, reps=3):
     per = []
     for c in calls:
         one(c)
+        torch.cuda._sleep(HOLD_CYCLES * reps)  # _hold, long enough for all reps' enqueues
         evs = []
         for _ in range(reps):
             s = torch.cuda.Event(enable_timing=True)
@@ -711,7 +729,8 @@ def _report(args, world, rank, mats, calls, ns, step_ms, value, chosen, launches
                                + " N=" + ",".join(map(str, ns)),
                    "matrices": [m["name"] for m in mats], "ns": ns,
                    "calls_per_step": len(calls), "selector": os.path.basename(args.model),
-                   "l2": "flushed before every timed call (read sweep of 256 MiB, clean lines)",
+                   "l2": "flushed before every timed call (read sweep of 256 MiB, clean lines), "
+                         "then a ~100 us device spin so the call is enqueued before it starts",
                    "parallelism": (f"{world} GPUs: calls sharded by multi.schedule_units (large calls "
                                    "as nnz-balanced row panels, B replicated; the rest whole, LPT)")
                                   if world > 1 else "1 GPU"},

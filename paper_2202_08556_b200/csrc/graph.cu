@@ -305,7 +305,9 @@ extern "C" int daspmm_spmm_selected(const daspmm_csr* h, const daspmm_model* m, 
     const bool reselect = (flags & DASPMM_RESELECT) != 0;
     const unsigned kflags = flags & ~unsigned(DASPMM_RESELECT);
     const DecisionKey dk{model_generation(m), N, uh ? hw : -1};
-    const Key key{model_generation(m), d_B, b_layout, ldb, N, d_C, ldc, W, kflags, uh ? hw : -1, s};
+    // The key keeps the RESELECT bit: a reselect graph never publishes its choice, so a
+    // plain call must not reuse it (it would never reach the direct steady state).
+    const Key key{model_generation(m), d_B, b_layout, ldb, N, d_C, ldc, W, flags, uh ? hw : -1, s};
 
     int decided = -1;
     Entry* en = nullptr;

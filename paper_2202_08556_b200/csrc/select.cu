@@ -24,6 +24,10 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "common.cuh"
 #include "exact_sum.cuh"
 #include "internal.h"
 
@@ -44,7 +48,9 @@ struct DevNode {
     double thr;   // std_row threshold (feature 2)
     long long icut;  // integer cut for features 0, 1, 3, 4
     double value;
+    double pad2;     // 48 bytes: runs of nodes are 16-B aligned for 1-D TMA staging
 };
+static_assert(sizeof(DevNode) == 48, "DevNode staged by cp.async.bulk in 16-B units");
 
 }  // namespace daspmm
 
@@ -365,15 +371,178 @@ k_select(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off
     }
 }
 
+// The same decision from a cluster of kSelCta CTAs: CTA q stages the nodes of its
+// contiguous run of trees into shared memory with coalesced 16-byte loads (one pass over
+// the model instead of a chain of dependent global loads per tree level), each thread
+// walks one tree there, and CTA 0 gathers the leaves through distributed shared memory
+// and sums them per class in round order (gbdt.hpp:60-65). Bits are those of k_select.
+// A std_row split inside the proven interval sends CTA 0 down k_select's path (exact
+// replay, then every tree walked again from global memory).
+constexpr int kSelCta = 8;
+struct SelRuns {  // node run [n[q], n[q+1]) of CTA q, from the host's tree offsets
+    long long n[kSelCta + 1];
+};
+
+__global__ void __cluster_dims__(kSelCta, 1, 1) __launch_bounds__(kSelThreads)
+k_select_cluster(const DevNode* __restrict__ nodes, const int64_t* __restrict__ tree_off,
+                 int num_rounds, int num_classes, int per_cta, int stage_nodes, SelRuns runs,
+                 const int* __restrict__ rp, DevFeatures* feat, long long n_cols, long long hw,
+                 int* out_kernel, cudaGraphConditionalHandle cond, int use_cond, int* cache,
+                 volatile int* publish) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned q = cluster.block_rank();
+    if (cache != nullptr) {  // every CTA reads the same value: only CTA 0 writes it, last
+        const int cached = *cache;
+        if (cached >= 0) {
+            if (q == 0 && threadIdx.x == 0) {
+                *out_kernel = cached;
+                if (publish != nullptr) *publish = cached;
+                if (use_cond) cudaGraphSetConditional(cond, unsigned(cached));
+            }
+            return;
+        }
+    }
+    extern __shared__ __align__(16) unsigned char sel_smem[];  // DevNode needs 8
+    // [stage_nodes DevNode][per_cta doubles: this CTA's leaves][ntrees doubles: CTA 0's]
+    DevNode* snodes = reinterpret_cast<DevNode*>(sel_smem);
+    double* my_leaf = reinterpret_cast<double*>(snodes + stage_nodes);
+    double* all_leaf = my_leaf + per_cta;
+    __shared__ int amb;
+    __shared__ int any_amb;
+    __shared__ double scores[kMaxClasses];
+    const int ntrees = num_rounds * num_classes;
+    const int t0 = min(int(q) * per_cta, ntrees), t1 = min(t0 + per_cta, ntrees);
+    const int64_t n0 = runs.n[q], n1 = runs.n[q + 1];
+    const bool staged = n1 - n0 <= stage_nodes;
+    if (threadIdx.x == 0) amb = 0;
+    __shared__ __align__(8) uint64_t bar;
+    // One 1-D TMA bulk copy of the CTA's node run (one elected thread, mbarrier
+    // completion); the first tree's root offset is loaded while it is in flight.
+    const unsigned bytes = unsigned(n1 - n0) * unsigned(sizeof(DevNode));
+    if (staged && threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    if (staged && threadIdx.x == 0 && bytes > 0) {
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(snodes, nodes + n0, bytes, &bar);
+    }
+    const int64_t root0 = t0 + int(threadIdx.x) < t1 ? __ldg(tree_off + t0 + threadIdx.x) : 0;
+    const long long nnz = feat->nnz > 1 ? feat->nnz : 1;
+    const long long rows = feat->rows > 1 ? feat->rows : 1;
+    const double lo = feat->std_lo, hi = feat->std_hi;
+    const bool have = feat->exact_valid != 0;
+    const double ex = feat->std_exact;
+    if (staged && bytes > 0) mbar_wait(&bar, 0);
+    for (int t = t0 + int(threadIdx.x); t < t1; t += blockDim.x) {
+        int64_t i = t == t0 + int(threadIdx.x) ? root0 : tree_off[t];  // absolute index
+        bool ambiguous = false;
+        while (true) {
+            const DevNode nd = staged ? snodes[i - n0] : nodes[i];
+            if (nd.feature < 0) break;
+            const int d = decide(nd, nnz, rows, n_cols, hw, lo, hi, have, ex);
+            if (d == 2) {
+                ambiguous = true;
+                break;
+            }
+            i = d ? nd.left : nd.right;
+        }
+        if (ambiguous) amb = 1;
+        else my_leaf[t - t0] = staged ? snodes[i - n0].value : nodes[i].value;
+    }
+    cluster.sync();  // every CTA's leaves and flag are in its shared memory
+    if (q == 0) {
+        if (threadIdx.x == 0) {
+            int a = 0;
+            for (unsigned r = 0; r < unsigned(kSelCta); ++r) a |= *cluster.map_shared_rank(&amb, r);
+            any_amb = a;
+        }
+        __syncthreads();
+        if (!any_amb) {
+            for (int t = threadIdx.x; t < ntrees; t += blockDim.x) {
+                const int r = t / per_cta;
+                all_leaf[t] = cluster.map_shared_rank(my_leaf, unsigned(r))[t - r * per_cta];
+            }
+        }
+    }
+    cluster.sync();  // the peers' shared memory may go away after this
+    if (q != 0) return;
+    if (any_amb) {
+        // Rare: replay the reference's sequential std_row sum (features.hpp:27-35) once,
+        // cache it, and walk every tree again with the exact value.
+        const int M = int(feat->rows);
+        const double ss = M > 0 ? exact_sequential_sum<kSelThreads>(rp, M, feat->mean) : 0.0;
+        const double sd = M > 0 ? __dsqrt_rn(__ddiv_rn(ss, double(M))) : 0.0;
+        if (threadIdx.x == 0) {
+            feat->std_exact = sd;
+            feat->exact_valid = 1;
+        }
+        for (int t = threadIdx.x; t < ntrees; t += blockDim.x) {
+            int64_t i = tree_off[t];
+            while (true) {
+                const DevNode nd = nodes[i];
+                if (nd.feature < 0) break;
+                i = decide(nd, nnz, rows, n_cols, hw, lo, hi, true, sd) ? nd.left : nd.right;
+            }
+            all_leaf[t] = nodes[i].value;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < num_classes) {
+        double s = 0.0;
+#pragma unroll 10
+        for (int r = 0; r < num_rounds; ++r) s = __dadd_rn(s, all_leaf[r * num_classes + threadIdx.x]);
+        scores[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int c = 1; c < num_classes; ++c)
+            if (scores[c] > scores[best]) best = c;
+        *out_kernel = best;
+        if (cache != nullptr) *cache = best;
+        if (publish != nullptr) *publish = best;
+        if (use_cond) cudaGraphSetConditional(cond, unsigned(best));
+    }
+}
+
 uint64_t model_generation(const daspmm_model* m) { return m->generation; }
 
 int launch_select(const daspmm_csr* h, const daspmm_model* m, int64_t n_cols, int64_t hw,
                   int* d_kernel, cudaGraphConditionalHandle cond, bool use_cond, cudaStream_t s,
                   int* cache, int* publish) {
     const int ntrees = int(m->rounds.size()) * m->num_classes;
-    const size_t smem = sizeof(double) * size_t(std::max(ntrees, 1));
     if (m->num_classes > kMaxClasses)
         return fail(DASPMM_ERR_UNSUPPORTED, "select: more than 16 classes");
+    // Cluster path: the largest per-CTA node run staged in shared memory (~100 KB for
+    // the shipped 100-round, depth-4, 8-class model); beyond 200 KB the CTAs walk their
+    // trees in global memory. DASPMM_SELECT_ONE_CTA=1 keeps the one-CTA kernel.
+    static const bool one_cta = [] {
+        const char* v = std::getenv("DASPMM_SELECT_ONE_CTA");
+        return v && v[0] == '1';
+    }();
+    if (!one_cta && ntrees >= kSelCta) {
+        const int per_cta = (ntrees + kSelCta - 1) / kSelCta;
+        int64_t most = 0;
+        SelRuns runs{};
+        for (int q = 0; q <= kSelCta; ++q)
+            runs.n[q] = m->tree_off[size_t(std::min(q * per_cta, ntrees))];
+        for (int q = 0; q < kSelCta; ++q) most = std::max<int64_t>(most, runs.n[q + 1] - runs.n[q]);
+        const size_t leaves = sizeof(double) * size_t(per_cta + ntrees);
+        int stage = int(most);
+        if (sizeof(DevNode) * size_t(stage) + leaves > 200 * 1024) stage = 0;
+        const size_t smem = sizeof(DevNode) * size_t(stage) + leaves;
+        if (smem <= 200 * 1024) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem));
+            k_select_cluster<<<kSelCta, kSelThreads, smem, s>>>(
+                m->d_nodes, m->d_tree_off, int(m->rounds.size()), m->num_classes, per_cta, stage,
+                runs, h->rp, h->d_feat, n_cols, hw, d_kernel, cond, use_cond ? 1 : 0, cache, publish);
+            cudaError_t e = cudaGetLastError();
+            return e == cudaSuccess ? DASPMM_OK : cuda_fail(e, "select");
+        }
+    }
+    const size_t smem = sizeof(double) * size_t(std::max(ntrees, 1));
     if (smem > 200 * 1024) return fail(DASPMM_ERR_UNSUPPORTED, "select: ensemble too large");
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

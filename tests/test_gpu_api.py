@@ -73,6 +73,24 @@ def test_selected_cache_stays_bounded(env):
     assert np.allclose(y, y64, rtol=1e-4, atol=1e-4)
 
 
+def test_plain_call_after_reselect_reaches_the_direct_path(env):
+    """A reselect call first (its graph never publishes), then plain calls on the same
+    operands: they must build their own publishing graph and reach the decided, direct
+    state rather than replay the reselect graph forever."""
+    torch, gen, sk, model = env
+    a = H.random_csr(3000, 2500, 40000, seed=77, skew=1.0)
+    d = _dev(env, a)
+    B = torch.rand(a.num_cols, 16, device="cuda")
+    C = torch.empty(a.num_rows, 16, device="cuda")
+    sk.spmm_selected(d, model, B, C, reselect=True)
+    torch.cuda.synchronize()
+    assert sk.selected_cache_info(d)[2] == 0
+    for _ in range(3):
+        sk.spmm_selected(d, model, B, C)
+        torch.cuda.synchronize()
+    assert sk.selected_cache_info(d)[2] == 1
+
+
 def test_reselect_equals_published_path(env):
     """DASPMM_RESELECT (selector walk + SWITCH every call) gives the same kernel and the
     same bits as the cached direct launch."""

@@ -326,6 +326,49 @@ def test_device_selector_bit_exact_with_host_predict(sk):
     assert n_checked >= 200
 
 
+def _std_split_model(thr):
+    """8 one-split trees on std_row (feature 2) at `thr`: class 0 wins when
+    std_row <= thr, class 1 otherwise (selector text v1, gbdt.hpp:336-453)."""
+    lines = ["spmmkit-selector v1", "uses_hardware 0", "spmmkit-gbdt v1",
+             "classes 8 features 4 best_round 0",
+             "config num_rounds 1 max_depth 1 min_leaf 1 learning_rate 0.10000000000000001 "
+             "patience 10 lambda 9.9999999999999995e-07 seed 0",
+             "feature_names 4 log2_nnz log2_mat_size std_row n_cols", "rounds 1"]
+    for c in range(8):
+        lo, hi = {0: (1.0, -1.0), 1: (-1.0, 1.0)}.get(c, (0.0, 0.0))
+        lines += [f"tree 0 {c} 3", f"node split 2 {thr!r} 1 2 1.0", f"node leaf {lo!r}",
+                  f"node leaf {hi!r}"]
+    return "\n".join(lines + ["end"]) + "\n"
+
+
+def test_device_selector_std_split_at_the_exact_value(sk):
+    """A std_row split exactly at (and one ulp below) the reference's std_row: the
+    device selector (cluster kernel, on a fresh handle whose exact std_row is not yet
+    known) must decide as the host's sequential double sum (features.hpp:27-35), going
+    through the exact replay when the threshold falls inside the proven interval."""
+    import math
+
+    import torch
+
+    out = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for seed, skew in ((1, 0.0), (2, 1.2), (3, 2.0)):
+        a = H.random_csr(5000, 5000, 60000, seed=seed, dtype=np.float32, skew=skew)
+        lens = np.diff(a.row_offsets)
+        M = a.num_rows
+        mean = float(int(a.row_offsets[-1])) / float(M)
+        acc = 0.0
+        for x in lens.tolist():
+            d = float(x) - mean
+            acc += d * d
+        std = math.sqrt(acc / M)
+        for thr, want in ((std, 0), (math.nextafter(std, -math.inf), 1),
+                          (math.nextafter(std, math.inf), 0)):
+            d = sk.DeviceCsr.from_host(a)  # fresh handle: no exact std_row cached yet
+            sk.select_device(d, sk.load_selector(_std_split_model(thr)), 32, out)
+            torch.cuda.synchronize()
+            assert int(out.item()) == want, (seed, thr, std)
+
+
 def test_graph_dispatch_runs_the_selected_kernel(sk):
     """spmm_selected: the SWITCH body that runs is the selector's choice, and the
     output equals spmm with that kernel; both B layouts; repeated calls reuse the graph."""

@@ -61,6 +61,7 @@ def time_kernel(fn, flush, reps=5):
     ts = []
     for _ in range(reps):
         flush.sum()  # clean lines: the timed call pays no write-back
+        torch.cuda._sleep(200_000)  # GPU busy until the call is enqueued (bench._hold)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
