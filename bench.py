@@ -436,7 +436,20 @@ def _batched_small(calls, model, flush, per_call_ms, reps=5, max_nnz=300_000):
         tot += s.elapsed_time(e)
     ms = tot / reps
     one_by_one = sum(per_call_ms[i] for i in idx)
+    # the floor of a one-by-one call: a minimal kernel between the same event pair, after
+    # the same flush and hold (launch + event latency with nothing to do)
+    floor = 0.0
+    for _ in range(reps):
+        _flush(flush)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.cuda._sleep(0)
+        e.record()
+        torch.cuda.synchronize()
+        floor += s.elapsed_time(e)
     return {"calls": len(idx), "graph_ms": round(ms, 4),
+            "empty_launch_us": round(floor / reps * 1e3, 2),
             "us_per_call": round(ms * 1e3 / len(idx), 2),
             "one_by_one_ms": round(one_by_one, 4),
             "one_by_one_us_per_call": round(one_by_one * 1e3 / len(idx), 2),
