@@ -363,10 +363,19 @@ def test_device_selector_std_split_at_the_exact_value(sk):
         std = math.sqrt(acc / M)
         for thr, want in ((std, 0), (math.nextafter(std, -math.inf), 1),
                           (math.nextafter(std, math.inf), 0)):
+            model = sk.load_selector(_std_split_model(thr))
             d = sk.DeviceCsr.from_host(a)  # fresh handle: no exact std_row cached yet
-            sk.select_device(d, sk.load_selector(_std_split_model(thr)), 32, out)
+            sk.select_device(d, model, 32, out)
             torch.cuda.synchronize()
             assert int(out.item()) == want, (seed, thr, std)
+            # the same decision inside the DA-SpMM graph (selector node -> SWITCH)
+            d = sk.DeviceCsr.from_host(a)
+            B = torch.rand(a.num_cols, 32, device="cuda")
+            C = torch.empty(a.num_rows, 32, device="cuda")
+            out.fill_(-1)
+            sk.spmm_selected(d, model, B, C, kernel_out=out)
+            torch.cuda.synchronize()
+            assert int(out.item()) == want, ("graph", seed, thr, std)
 
 
 def test_graph_dispatch_runs_the_selected_kernel(sk):
