@@ -384,10 +384,15 @@ def run_ours(args):
 
     # ---- e2e: host operands through the public API (pinned H2D, DA-SpMM, D2H)
     e2e = parity = warm = overhead = batched = setup = None
+    # operands too large to stage in pinned host memory (c5: 68 GB) skip e2e; decided on
+    # the largest rank's operands so every rank takes the same branch (_e2e has collectives)
+    op_bytes = float(sum(c["B"].numel() + c["C"].numel() for c in calls) * 4)
+    if world > 1:
+        op_bytes = _max_over_ranks(op_bytes, dev)
     if args.profile_step:
         pass  # --profile-step: only the warm-up and the timed steps (ncu launch lists)
-    elif sum(c["B"].numel() + c["C"].numel() for c in calls) * 4 > (16 << 30):
-        e2e = None  # operands too large to stage in pinned host memory (c5: 68 GB)
+    elif op_bytes > (16 << 30):
+        e2e = None
     else:
         e2e = _e2e(calls, one, stream, args, world, total_flops)
     if not args.profile_step:

@@ -204,3 +204,29 @@ def test_fused_rows_allgather_two_gpus():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count("equals single-GPU C: True") == 2, r.stdout
+
+
+def test_bench_two_ranks_under_torchrun():
+    """The driver's N>1 launch of bench.py (torch.distributed.run, one process per rank)
+    on a 1-GPU box: both ranks on cuda:0 over gloo (NCCL refuses two ranks on one GPU).
+    Rank 0 prints one JSON line for the whole job; the other exits 0."""
+    import json
+    import subprocess
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, DASPMM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--small", "--no-cpu", "--no-cusparse"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 2
+    assert d["e2e"] is not None and d["e2e"]["value"] > 0
+    assert d["parity"]["calls_passed"] == d["parity"]["calls_checked"] > 0
