@@ -34,7 +34,8 @@ def main():
         agg = {k: v for k, v in agg.items() if k.startswith("daspmm::")}
     if "--step" in sys.argv:
         setup = ("k_row_terms", "k_cols_touched", "k_popcount", "k_fine_spans", "k_coo_rows",
-                 "k_tile_spans", "k_tile_fill", "k_std_sequential", "k_ingest", "k_rebase")
+                 "k_tile_spans", "k_tile_fill", "k_std_sequential", "k_ingest", "k_rebase",
+                 "k_rows_unsorted", "k_tile_windows", "k_spans_init")
         agg = {k: v for k, v in agg.items() if not any(f"::{n}" in k for n in setup)}
     tot = sum(v[1] for v in agg.values()) or 1.0
     print(f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}")
