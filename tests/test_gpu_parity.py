@@ -896,3 +896,38 @@ def test_exact_std_block_sum_matches_sequential(sk, case):
             want = O.extract_features(O.Csr(M, 1, rp, ci, np.ones(nnz)))[2]
             assert got == want, (case, M, got, want)
         d.close()
+
+
+_ONE_CTA_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import numpy as np, torch
+import helpers as H
+from paper_2202_08556_b200 import spmmkit as sk
+m = sk.load_selector(open(os.path.join(os.path.dirname(sk.__file__), "models",
+                                       "b200_selector.txt")).read())
+out = torch.zeros(1, dtype=torch.int32, device="cuda")
+for seed in range(6):
+    a = H.random_csr(3000, 3000, 3000 * (3 + seed), seed=seed, dtype=np.float32,
+                     skew=[0.0, 1.2][seed % 2])
+    d = sk.DeviceCsr.from_host(a)
+    for n in (2, 16, 128):
+        sk.select_device(d, m, n, out)
+        torch.cuda.synchronize()
+        assert int(out.item()) == sk.predict_kernel(m, sk.extract_features(d, n)).index()
+print("one-cta ok")
+"""
+
+
+def test_one_cta_selector_matches_host_predict(sk):
+    """DASPMM_SELECT_ONE_CTA=1 (read once per process, so in a subprocess): the one-CTA
+    selector kernel decides as the host's predict_kernel, like the cluster kernel."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DASPMM_SELECT_ONE_CTA="1", ROOT=root)
+    r = subprocess.run([sys.executable, "-c", _ONE_CTA_SCRIPT], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=root)
+    assert r.returncode == 0 and "one-cta ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
