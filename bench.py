@@ -129,7 +129,7 @@ HOLD_CYCLES = 200_000  # ~100 us at 1965 MHz
 def _hold():
     """A ~100 us device spin on the launching stream before a timed call's start event,
     so the host's per-call work (operand checks, ctypes, event records) can never land
-    inside the event pair on an idle GPU. Measured (tools/experiments/small_call_probe.py,
+    inside the event pair on an idle GPU. Measured (tools/experiments/small_call_hold_probe.py,
     profiles/r02e_small_call_probe.txt): the per-call times are the same with and without
     it apart from the first call of a handle, so it is a guard, not a correction. The
     spin touches no memory, so the flushed L2 state is unchanged."""
