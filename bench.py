@@ -182,6 +182,7 @@ def _setup_costs(mats):
     """Handle-creation cost per matrix (not in any timed SpMM): device arrays adopted
     (features, empty rows, K_touched, column windows: daspmm_csr_create_device), host int64
     arrays uploaded and validated / compacted on the device (daspmm_csr_create_host),
+    shuffled device COO triplets sorted and merged on the device (from_coo),
     extract_features' exact std_row replay, and what the first calls build lazily (COO
     row ids; the row-panel tiles where they pay)."""
     import numpy as np
@@ -228,8 +229,24 @@ def _setup_costs(mats):
             torch.cuda.synchronize()
             t_lazy.append(((t1 - t0) - (time.perf_counter() - t1)) * 1e3)
             h.close()
+        # from shuffled device COO triplets (daspmm_csr_create_coo_device: sort, merge,
+        # offsets on the device, then the same handle set-up as from_device)
+        rows = torch.repeat_interleave(torch.arange(m["M"], device="cuda"),
+                                       (m["rp"][1:] - m["rp"][:-1]).long())
+        perm = torch.randperm(rows.numel(), device="cuda")
+        cr, cc, cv = rows[perm], m["ci"].long()[perm], m["va"][perm]
+        t_coo = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hc = sk.DeviceCsr.from_coo_device(m["M"], m["K"], cr, cc, cv)
+            torch.cuda.synchronize()
+            t_coo.append((time.perf_counter() - t0) * 1e3)
+            hc.close()
+        del rows, perm, cr, cc, cv
         t_host, t_feat, t_lazy = sorted(t_host)[1], sorted(t_feat)[1], sorted(t_lazy)[1]
         out[m["name"]] = {"from_device_ms": round(sorted(t_dev)[1], 3),
+                          "from_coo_device_ms": round(sorted(t_coo)[1], 3),
                           "from_host_ms": round(t_host, 3),
                           "extract_features_exact_ms": round(t_feat, 3),
                           "first_call_lazy_build_ms": round(t_lazy, 3),

@@ -100,6 +100,17 @@ int daspmm_csr_create_device(int64_t num_rows, int64_t num_cols, int64_t nnz,
                              const void* d_values, int dtype, int copy, daspmm_stream stream,
                              daspmm_csr** out);
 
+/* CsrMatrix::from_coo on the device (types.hpp:54-90): triplets (int64 row, int64 col,
+ * value) in device memory, any order; out-of-bounds coordinates fail with the
+ * reference's message; duplicate coordinates are summed (left to right in input order —
+ * the reference's std::sort leaves their order unspecified; inputs without duplicates
+ * give exactly from_coo's CSR). The handle owns the built arrays. Stream-ordered, with
+ * two host synchronisations (bounds verdict, output size). */
+int daspmm_csr_create_coo_device(int64_t num_rows, int64_t num_cols, int64_t n_triplets,
+                                 const int64_t* d_rows, const int64_t* d_cols,
+                                 const void* d_values, int dtype, daspmm_stream stream,
+                                 daspmm_csr** out);
+
 /* The values of a borrowed CSR were changed in place (same structure): drops the
  * handle's derived copies of the values (row-panel tiles, rebuilt on the next call that
  * uses them). Synchronises the handle's device first. */

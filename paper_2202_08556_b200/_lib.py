@@ -40,6 +40,8 @@ SIGNATURES = {
     "daspmm_csr_create_host": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.POINTER(_vp)]),
     "daspmm_csr_create_device": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.c_int, _vp,
                                            C.POINTER(_vp)]),
+    "daspmm_csr_create_coo_device": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int, _vp,
+                                               C.POINTER(_vp)]),
     "daspmm_csr_create_panel": (C.c_int, [_vp, _i64, _i64, _vp, C.POINTER(_vp)]),
     "daspmm_csr_destroy": (C.c_int, [_vp]),
     "daspmm_csr_values_updated": (C.c_int, [_vp]),

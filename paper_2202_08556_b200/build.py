@@ -31,7 +31,7 @@ CFLAGS = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcom
 
 LIB_SOURCES = ["abi.cu", "features.cu", "select.cu", "graph.cu", "spmm_rb_sr.cu",
                "spmm_rb_pr.cu", "spmm_eb_sr.cu", "spmm_eb_pr.cu", "spmm_lean.cu", "spmm_tma.cu",
-               "multi.cu", "spmm_pr_wide.cu", "spmm_tile.cu", "spmm_cm.cu"]
+               "multi.cu", "spmm_pr_wide.cu", "spmm_tile.cu", "spmm_cm.cu", "coo.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "dispatch.h", "internal.h", "launch_sr.cuh",
            "launch_pr.cuh", "lean.cuh", "tma_gather.cuh", "tile.cuh", "exact_sum.cuh"]
 

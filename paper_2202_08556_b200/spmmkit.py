@@ -280,6 +280,25 @@ class DeviceCsr:
         keep = None if copy else (row_offsets, col_indices, values)
         return DeviceCsr(out.value, dtype, keep, row_offsets.device.index)
 
+    @staticmethod
+    def from_coo_device(num_rows, num_cols, rows, cols, values, stream=None) -> "DeviceCsr":
+        """CsrMatrix::from_coo (types.hpp:54-90) on the device: torch int64 row / column
+        tensors and float32/float64 values on the GPU, any order; duplicates summed in
+        input order; out-of-bounds coordinates raise InvalidArgument with the reference's
+        message (daspmm_csr_create_coo_device)."""
+        import torch
+
+        assert rows.dtype == torch.int64 and cols.dtype == torch.int64
+        assert rows.numel() == cols.numel() == values.numel()
+        dtype = np.float32 if values.dtype == torch.float32 else np.float64
+        rows, cols, values = rows.contiguous(), cols.contiguous(), values.contiguous()
+        out = C.c_void_p()
+        check(lib().daspmm_csr_create_coo_device(num_rows, num_cols, rows.numel(),
+                                                 rows.data_ptr(), cols.data_ptr(),
+                                                 values.data_ptr(), _dtype_code(dtype),
+                                                 _stream_ptr(stream), C.byref(out)))
+        return DeviceCsr(out.value, dtype, None, rows.device.index)
+
     def values_updated(self):
         """The borrowed values tensor was changed in place (same structure): drop the
         handle's derived copies of the values (daspmm_csr_values_updated)."""

@@ -334,3 +334,51 @@ def test_concurrent_host_threads_share_a_handle(env):
         bound = H.gamma_bound(a, x64, np.float32)
         assert (np.abs(y1 - y64) <= bound).all(), tid
         assert (np.abs(y2 - y64) <= bound).all(), tid
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_from_coo_device_matches_host_from_coo(env, dtype):
+    """daspmm_csr_create_coo_device == CsrMatrix::from_coo (types.hpp:54-90, host mirror
+    in spmmkit.py): shuffled triplets with duplicates (summed in input order), empty
+    rows, out-of-bounds coordinates rejected with the reference's message. Checked bit
+    for bit by multiplying with an identity B (C = A densified) and against the oracle."""
+    torch, gen, sk, model = env
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    rng = np.random.default_rng(11)
+    M, K, n = 600, 500, 9000
+    r = rng.integers(0, M - 50, n)          # the last 50 rows stay empty
+    c = rng.integers(0, K, n)
+    dup = rng.integers(0, n, 1500)           # repeated coordinates
+    r = np.concatenate([r, r[dup]])
+    c = np.concatenate([c, c[dup]])
+    v = rng.uniform(-1, 1, r.size).astype(dtype)
+    host = sk.CsrMatrix.from_coo(M, K, list(zip(r.tolist(), c.tolist(), v.tolist())), dtype)
+    d = sk.DeviceCsr.from_coo_device(M, K, torch.tensor(r, device="cuda"),
+                                     torch.tensor(c, device="cuda"),
+                                     torch.tensor(v, device="cuda"))
+    assert d.nnz() == host.nnz() and d.empty_rows >= 50
+    eye = torch.eye(K, dtype=tdt, device="cuda")
+    out = torch.empty(M, K, dtype=tdt, device="cuda")
+    sk.spmm_device(0, d, eye, out, exact=True)
+    dense = np.zeros((M, K), dtype)
+    for i in range(M):
+        s, e = host.row_offsets[i], host.row_offsets[i + 1]
+        dense[i, host.col_indices[s:e]] = host.values[s:e]
+    got = out.cpu().numpy()
+    assert np.array_equal(got, dense)
+    # the handle computes like any other: RB+RM+SR vs the oracle
+    B = torch.rand(K, 16, dtype=tdt, device="cuda")
+    C = torch.empty(M, 16, dtype=tdt, device="cuda")
+    sk.spmm_device(4, d, B, C)
+    x = B.cpu().numpy().astype(np.float64)
+    y64 = O.spmm_reference(H.to_oracle(host), x)
+    assert np.all(np.abs(C.cpu().numpy() - y64) <= H.gamma_bound(host, x, dtype))
+    # errors and the empty input
+    with pytest.raises(sk.InvalidArgument, match="from_coo: coordinate out of bounds"):
+        sk.DeviceCsr.from_coo_device(M, K, torch.tensor([0, M], device="cuda"),
+                                     torch.tensor([0, 0], device="cuda"),
+                                     torch.ones(2, dtype=tdt, device="cuda"))
+    e = sk.DeviceCsr.from_coo_device(M, K, torch.zeros(0, dtype=torch.int64, device="cuda"),
+                                     torch.zeros(0, dtype=torch.int64, device="cuda"),
+                                     torch.zeros(0, dtype=tdt, device="cuda"))
+    assert e.nnz() == 0 and e.empty_rows == M
