@@ -403,7 +403,7 @@ k_select_cluster(const DevNode* __restrict__ nodes, const int64_t* __restrict__ 
             return;
         }
     }
-    extern __shared__ __align__(16) unsigned char sel_smem[];  // DevNode needs 8
+    extern __shared__ __align__(16) unsigned char sel_smem[];  // TMA destination: 16-B aligned
     // [stage_nodes DevNode][per_cta doubles: this CTA's leaves][ntrees doubles: CTA 0's]
     DevNode* snodes = reinterpret_cast<DevNode*>(sel_smem);
     double* my_leaf = reinterpret_cast<double*>(snodes + stage_nodes);
