@@ -623,8 +623,12 @@ def _assembly(calls, mats, world, dev):
            else "all-gather of padded row panels (multi.gather_rows)"}
     # Fused alternative (NCCL runs only, one rank per GPU): the RB+RM+SR panel kernel
     # stores every finished row into all ranks' copies of C (symmetric memory over
-    # NVLink); its time includes the SpMM itself.
-    if dist.get_backend() == "nccl" and not by_cols:
+    # NVLink); its time includes the SpMM itself. Opt-in (DASPMM_BENCH_FUSED=1): it meets
+    # at device-side symmetric-memory barriers, which would spin if one rank failed
+    # before them, and it has not yet run on a multi-GPU box — the default multi-GPU
+    # bench line must not depend on it.
+    if dist.get_backend() == "nccl" and not by_cols and \
+            os.environ.get("DASPMM_BENCH_FUSED") == "1":
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
